@@ -1,0 +1,156 @@
+/*
+ * octoquant_b200.h — C ABI of the B200-native OCTOPUS KV-cache codec hot path.
+ *
+ * This is the drop-in boundary for the reference's C++ API in
+ * /root/reference/proj/include/octoquant (a header-only CPU library).  Every
+ * entry point below names the reference interface it replaces.  Signatures
+ * carry plain pointers and sizes only (no torch or CUDA types; a CUDA stream
+ * is passed as `void*`, NULL = legacy default stream).  Device pointers are
+ * caller-owned; an oq_codec owns only its codebook tables.
+ *
+ * Error behaviour mirrors the reference's exceptions:
+ *   OQ_ERR_INVALID_ARGUMENT  <-> std::invalid_argument (config / shape errors)
+ *   OQ_ERR_FORMAT            <-> octoquant::FormatError (corrupt codes / wire)
+ * plus OQ_ERR_CUDA / OQ_ERR_UNSUPPORTED.  oq_last_error() returns the
+ * thread-local message of the last failure.  There is no CPU fallback: with
+ * no usable CUDA device the device entry points return OQ_ERR_CUDA.
+ */
+#ifndef OCTOQUANT_B200_H
+#define OCTOQUANT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  OQ_OK = 0,
+  OQ_ERR_INVALID_ARGUMENT = 1,
+  OQ_ERR_FORMAT = 2,
+  OQ_ERR_CUDA = 3,
+  OQ_ERR_UNSUPPORTED = 4
+} oq_status;
+
+/* Rounding (codec.hpp:34) */
+enum { OQ_ROUND_SCALAR = 0, OQ_ROUND_LOCAL2X2 = 1, OQ_ROUND_LOCAL3X3 = 2, OQ_ROUND_FULL = 3 };
+/* Input element types accepted by oq_compress. */
+enum { OQ_DTYPE_F32 = 0, OQ_DTYPE_F64 = 1, OQ_DTYPE_F16 = 2, OQ_DTYPE_BF16 = 3 };
+/* Cache roles for the attention tile formats. */
+enum { OQ_ROLE_K = 0, OQ_ROLE_V = 1 };
+
+/* CodecConfig (codec.hpp:54-73), same fields and defaults. */
+typedef struct oq_config {
+  uint32_t dim;           /* 128 */
+  uint8_t b_dir;          /* 3 */
+  uint8_t b_nrm;          /* 1 */
+  uint8_t rounding;       /* OQ_ROUND_LOCAL3X3 */
+  uint8_t qjl;            /* 0 */
+  uint64_t rotation_seed; /* 0 */
+  uint64_t qjl_seed;      /* 1 */
+} oq_config;
+
+typedef struct oq_codec oq_codec;
+
+const char* oq_last_error(void);
+const char* oq_version(void);
+
+/* ---- configuration (codec.hpp:34-80, 351-356) ---------------------------- */
+oq_status oq_config_default(oq_config* cfg);                       /* CodecConfig{} */
+oq_status oq_config_validate(const oq_config* cfg);                /* codec.hpp:65-72 */
+oq_status oq_default_bit_split(int b, int* b_dir, int* b_nrm);     /* codec.hpp:77-80 */
+oq_status oq_parse_rounding(const char* name, int* rounding);      /* codec.hpp:45-52 */
+const char* oq_rounding_name(int rounding);                        /* codec.hpp:36-43 */
+double oq_effective_bits_per_coord(const oq_config* cfg);          /* codec.hpp:351-356 */
+size_t oq_record_bytes(const oq_config* cfg);                      /* codec.hpp:427-430 */
+
+/* ---- codebook construction (books.hpp:69-95, lloydmax.hpp:84-236) ------- */
+/* Host fp64 centroids (2^bits) and boundaries (2^bits - 1), bit-identical
+ * to the reference registry. */
+oq_status oq_xi_book(int bits, double* centroids, double* boundaries);
+oq_status oq_rho_book(uint32_t dim, int bits, double* centroids, double* boundaries);
+
+/* ---- Encoder(cfg) / Encoder(cfg, Books::custom(xi, rho))  codec.hpp:197-212 */
+/* Builds (or reuses) the books, derives the device tables and uploads them to
+ * the current CUDA device. */
+oq_status oq_codec_create(const oq_config* cfg, oq_codec** out);
+oq_status oq_codec_create_custom(const oq_config* cfg, const double* xi_centroids, int xi_bits,
+                                 const double* rho_centroids, int rho_bits, oq_codec** out);
+void oq_codec_destroy(oq_codec* codec);
+oq_status oq_codec_config(const oq_codec* codec, oq_config* cfg);
+
+/* ---- compress: Encoder::encode (codec.hpp:214-249) ----------------------
+ * x: device [n, dim] of `dtype`; records: device, n * oq_record_bytes bytes,
+ * written as the OCTO v1 per-key payload (codec.hpp:381-393) — the bytes
+ * pack_keys emits after its 20-byte header.  Codes are bit-exact vs the
+ * fp64 reference. */
+oq_status oq_compress(const oq_codec* codec, const void* x, int dtype, size_t n, void* records,
+                      void* stream);
+
+/* ---- decode: Encoder::decode (codec.hpp:268-275) -------------------------
+ * records -> out device [n, dim] fp32. */
+oq_status oq_decode(const oq_codec* codec, const void* records, size_t n, float* out,
+                    void* stream);
+
+/* ---- wire: pack_keys / unpack_keys (codec.hpp:364-478) -------------------
+ * An OCTO v1 blob is oq_wire_header(...) followed by the records. */
+oq_status oq_wire_header(const oq_config* cfg, uint64_t count, uint8_t header[20]);
+/* Checks magic/version/flags/bits/dim and the exact payload size
+ * (codec.hpp:411-430); fills cfg (rounding/seeds left at defaults). */
+oq_status oq_wire_parse_header(const uint8_t* blob, size_t nbytes, oq_config* cfg,
+                               uint64_t* count);
+/* Zero-padding checks of every record on the device (codec.hpp:447,455,459-461);
+ * synchronizes `stream`; OQ_ERR_FORMAT on a violation. */
+oq_status oq_validate_records(const oq_codec* codec, const void* records, size_t n,
+                              void* stream);
+
+/* ---- compressed-cache attention (attention.hpp:50-73) --------------------
+ * Batched GQA decode: q [B, Hq, dim] fp32 against B x Hkv compressed streams;
+ * q head h reads kv head h / (Hq / Hkv).  K and V are each compressed with
+ * their own codec (V with the same OCTOPUS codec, no QJL) and stored in the
+ * attention tile formats (oq_cache_pack).  out [B, Hq, dim] fp32 =
+ * softmax(score(q, k_t) / sqrt(dim)) . decode(v_t), the reference's
+ * attention_decode(enc_k, q, keys, Matrix{enc_v.decode(v)}, n_splits). */
+typedef struct oq_attn_shape {
+  int32_t B, Hq, Hkv;
+  uint64_t T;             /* tokens per sequence (max when seq_lens != NULL) */
+  uint64_t cap_tokens;    /* tokens allocated per (b, kv head) stream in the caches */
+  const int32_t* seq_lens;/* optional device [B] lengths (<= T), NULL = all T */
+} oq_attn_shape;
+
+size_t oq_cache_tile_bytes(const oq_codec* codec, int role); /* bytes per 32-token tile */
+size_t oq_cache_bytes(const oq_codec* codec, int role, uint64_t tokens); /* per stream */
+/* records: device [n_streams][rec_stride_tokens] records of n_tokens each
+ * -> tiles: device [n_streams][cap_tokens/32 tiles]. */
+oq_status oq_cache_pack(const oq_codec* codec, int role, const void* records, uint64_t n_streams,
+                        uint64_t n_tokens, uint64_t rec_stride_tokens, void* tiles,
+                        uint64_t cap_tokens, void* stream);
+size_t oq_attention_workspace_bytes(const oq_codec* ck, const oq_codec* cv,
+                                    const oq_attn_shape* shape, int n_splits);
+oq_status oq_attention_decode(const oq_codec* ck, const oq_codec* cv, const oq_attn_shape* shape,
+                              const float* q, const void* kcache, const void* vcache,
+                              float* out, int n_splits, void* workspace, size_t ws_bytes,
+                              void* stream);
+/* Sequence sharding: the SoftmaxState (m, l, acc) of tokens [t_begin, t_end)
+ * per (b, q head) -> partial [B*Hq][4 + dim] fp32 = (m, l, 0, 0, acc[dim]),
+ * m being the running max of log2-scaled logits and acc in the rotated V
+ * frame.  Chunks merge with oq_attention_combine in token order, which is
+ * the reference's SoftmaxState::merge (attention.hpp:36-44). */
+oq_status oq_attention_partials(const oq_codec* ck, const oq_codec* cv,
+                                const oq_attn_shape* shape, const float* q, const void* kcache,
+                                const void* vcache, uint64_t t_begin, uint64_t t_end,
+                                float* partial, int n_splits, void* workspace, size_t ws_bytes,
+                                void* stream);
+/* partials[row * row_stride + part * part_stride + (m, l, 0, 0, acc...)] for
+ * rows = B*Hq and n_parts chunks in token order -> out [rows][dim]
+ * (finalize: acc/l with the inverse V rotation applied) or, with
+ * finalize = 0, the merged partial [rows][4 + dim]. */
+oq_status oq_attention_combine(const oq_codec* cv, const float* partials, int rows, int n_parts,
+                               size_t row_stride, size_t part_stride, int finalize, float* out,
+                               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,457 @@
+"""B200-native OCTOPUS KV-cache codec hot path (arXiv 2605.21226).
+
+Python mirror of the reference C++ API (/root/reference/proj/include/octoquant)
+over the C ABI in ``include/octoquant_b200.h``.  Names, argument meaning and
+error behaviour follow the reference:
+
+==========================  =================================================
+reference (C++)             here
+==========================  =================================================
+CodecConfig / validate      :class:`CodecConfig` / ``.validate()``
+default_bit_split           :func:`default_bit_split`
+Rounding, parse_rounding    :data:`ROUNDINGS`, :func:`parse_rounding`
+xi_book / rho_book          :func:`xi_book`, :func:`rho_book`
+Encoder(cfg[, Books])       :class:`Encoder` (device tables on the current GPU)
+Encoder::encode             :meth:`Encoder.compress` (batched, bit-exact)
+Encoder::decode             :meth:`Encoder.decode`
+pack_keys / unpack_keys     :func:`pack_keys`, :func:`unpack_keys`
+attention_decode            :func:`attention_decode` (batched GQA, K and V
+                            compressed, split-K) + :class:`KVCache`
+std::invalid_argument       :class:`ValueError`
+FormatError                 :class:`FormatError`
+==========================  =================================================
+
+PyTorch is used only for device memory and streams.  There is no CPU compute
+path: every data-path call launches the sm_100a kernels in
+``liboctoquant_b200.so`` and fails loudly when the library or a GPU is absent.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = [
+    "CodecConfig", "Encoder", "FormatError", "KVCache", "ROUNDINGS", "attention_decode",
+    "attention_partials", "attention_combine", "default_bit_split",
+    "effective_bits_per_coord", "lib", "pack_keys", "parse_rounding", "record_bytes", "rho_book",
+    "unpack_keys", "xi_book",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liboctoquant_b200.so")
+
+ROUNDINGS = ("scalar", "local2x2", "local3x3", "full")
+ROLE_K, ROLE_V = 0, 1
+_DTYPES = {"float32": 0, "float64": 1, "float16": 2, "bfloat16": 3}
+
+
+class FormatError(RuntimeError):
+    """Corrupt codes or wire data (octoquant::FormatError, io.hpp:17-20)."""
+
+
+class _Config(C.Structure):
+    _fields_ = [("dim", C.c_uint32), ("b_dir", C.c_uint8), ("b_nrm", C.c_uint8),
+                ("rounding", C.c_uint8), ("qjl", C.c_uint8), ("rotation_seed", C.c_uint64),
+                ("qjl_seed", C.c_uint64)]
+
+
+class _Shape(C.Structure):
+    _fields_ = [("B", C.c_int32), ("Hq", C.c_int32), ("Hkv", C.c_int32), ("T", C.c_uint64),
+                ("cap_tokens", C.c_uint64), ("seq_lens", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load liboctoquant_b200.so (built in-tree by ``make``); raise if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `make` (or __graft_entry__.build()); "
+                          "there is no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    vp, sz, u64, i32 = C.c_void_p, C.c_size_t, C.c_uint64, C.c_int
+    cfgp = C.POINTER(_Config)
+    dp = C.POINTER(C.c_double)
+    L.oq_last_error.restype = C.c_char_p
+    L.oq_version.restype = C.c_char_p
+    sigs = {
+        "oq_config_validate": ([cfgp], i32),
+        "oq_default_bit_split": ([i32, C.POINTER(i32), C.POINTER(i32)], i32),
+        "oq_parse_rounding": ([C.c_char_p, C.POINTER(i32)], i32),
+        "oq_effective_bits_per_coord": ([cfgp], C.c_double),
+        "oq_record_bytes": ([cfgp], sz),
+        "oq_xi_book": ([i32, dp, dp], i32),
+        "oq_rho_book": ([C.c_uint32, i32, dp, dp], i32),
+        "oq_codec_create": ([cfgp, C.POINTER(vp)], i32),
+        "oq_codec_create_custom": ([cfgp, dp, i32, dp, i32, C.POINTER(vp)], i32),
+        "oq_codec_destroy": ([vp], None),
+        "oq_compress": ([vp, vp, i32, sz, vp, vp], i32),
+        "oq_decode": ([vp, vp, sz, vp, vp], i32),
+        "oq_wire_header": ([cfgp, u64, C.c_char_p], i32),
+        "oq_wire_parse_header": ([C.c_char_p, sz, cfgp, C.POINTER(u64)], i32),
+        "oq_validate_records": ([vp, vp, sz, vp], i32),
+        "oq_cache_tile_bytes": ([vp, i32], sz),
+        "oq_cache_bytes": ([vp, i32, u64], sz),
+        "oq_cache_pack": ([vp, i32, vp, u64, u64, u64, vp, u64, vp], i32),
+        "oq_attention_workspace_bytes": ([vp, vp, C.POINTER(_Shape), i32], sz),
+        "oq_attention_decode": ([vp, vp, C.POINTER(_Shape), vp, vp, vp, vp, i32, vp, sz, vp],
+                                i32),
+        "oq_attention_partials": ([vp, vp, C.POINTER(_Shape), vp, vp, vp, u64, u64, vp, i32, vp,
+                                   sz, vp], i32),
+        "oq_attention_combine": ([vp, vp, i32, i32, sz, sz, i32, vp, vp], i32),
+    }
+    for name, (args, res) in sigs.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(status):
+    if status == 0:
+        return
+    msg = lib().oq_last_error().decode()
+    if status == 1:
+        raise ValueError(msg)
+    if status == 2:
+        raise FormatError(msg)
+    if status == 4:
+        raise NotImplementedError(msg)
+    raise RuntimeError(f"CUDA error: {msg}")
+
+
+def _stream(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+@dataclass
+class CodecConfig:
+    """CodecConfig (codec.hpp:54-73), same fields and defaults."""
+    dim: int = 128
+    b_dir: int = 3
+    b_nrm: int = 1
+    rounding: str = "local3x3"
+    rotation_seed: int = 0
+    qjl: bool = False
+    qjl_seed: int = 1
+
+    def n_tri(self):
+        return (self.dim + 2) // 3
+
+    def _c(self):
+        if self.rounding not in ROUNDINGS:
+            raise ValueError(f"unknown rounding mode: {self.rounding}")
+        return _Config(self.dim, self.b_dir, self.b_nrm, ROUNDINGS.index(self.rounding),
+                       1 if self.qjl else 0, self.rotation_seed, self.qjl_seed)
+
+    def validate(self):
+        c = self._c()
+        _check(lib().oq_config_validate(C.byref(c)))
+
+    @staticmethod
+    def for_bits(b, **kw):
+        bd, bn = default_bit_split(b)
+        return CodecConfig(b_dir=bd, b_nrm=bn, **kw)
+
+
+def default_bit_split(b):
+    """codec.hpp:77-80: (b_dir, b_nrm) = (b + 1, b - 1)."""
+    bd, bn = C.c_int(), C.c_int()
+    _check(lib().oq_default_bit_split(int(b), C.byref(bd), C.byref(bn)))
+    return bd.value, bn.value
+
+
+def parse_rounding(name):
+    r = C.c_int()
+    _check(lib().oq_parse_rounding(name.encode(), C.byref(r)))
+    return ROUNDINGS[r.value]
+
+
+def effective_bits_per_coord(cfg: CodecConfig):
+    c = cfg._c()
+    return lib().oq_effective_bits_per_coord(C.byref(c))
+
+
+def record_bytes(cfg: CodecConfig):
+    c = cfg._c()
+    return lib().oq_record_bytes(C.byref(c))
+
+
+def _book(fn, *args, bits):
+    c = np.empty(1 << bits)
+    b = np.empty(max(1, (1 << bits) - 1))
+    _check(fn(*args, bits, c.ctypes.data_as(C.POINTER(C.c_double)),
+              b.ctypes.data_as(C.POINTER(C.c_double))))
+    return c, b[: (1 << bits) - 1]
+
+
+def xi_book(bits):
+    """books.hpp:69-74 -> (centroids, boundaries), bit-identical fp64."""
+    return _book(lib().oq_xi_book, bits=bits)
+
+
+def rho_book(dim, bits):
+    """books.hpp:86-95 -> (centroids, boundaries), bit-identical fp64."""
+    return _book(lib().oq_rho_book, dim, bits=bits)
+
+
+class Encoder:
+    """Encoder(cfg) / Encoder(cfg, Books::custom(xi, rho)) on the current GPU."""
+
+    def __init__(self, cfg: CodecConfig, books=None):
+        self.cfg = cfg
+        c = cfg._c()
+        h = C.c_void_p()
+        if books is None:
+            _check(lib().oq_codec_create(C.byref(c), C.byref(h)))
+        else:
+            xc = np.ascontiguousarray(books[0], np.float64)
+            rc = np.ascontiguousarray(books[1], np.float64)
+            xb = int(np.log2(len(xc)))
+            rb = int(np.log2(len(rc)))
+            if (1 << xb) != len(xc) or (1 << rb) != len(rc):
+                raise ValueError("custom books must have 2^bits centroids")
+            dp = C.POINTER(C.c_double)
+            _check(lib().oq_codec_create_custom(C.byref(c), xc.ctypes.data_as(dp), xb,
+                                                rc.ctypes.data_as(dp), rb, C.byref(h)))
+        self._h = h
+        self.record_bytes = record_bytes(cfg)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.oq_codec_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def config(self):
+        return self.cfg
+
+    def compress(self, x, out=None, stream=None):
+        """Encoder::encode over rows of a CUDA tensor -> uint8 [n, record_bytes]."""
+        import torch
+        if not x.is_cuda:
+            raise ValueError("compress expects a CUDA tensor (there is no CPU path)")
+        if x.shape[-1] != self.cfg.dim:
+            raise ValueError("key dimension mismatch")
+        x = x.contiguous()
+        n = x.numel() // self.cfg.dim
+        dt = _DTYPES.get(str(x.dtype).replace("torch.", ""))
+        if dt is None:
+            raise ValueError(f"unsupported dtype {x.dtype}")
+        if out is None:
+            out = torch.empty((n, self.record_bytes), dtype=torch.uint8, device=x.device)
+        _check(lib().oq_compress(self._h, _ptr(x), dt, n, _ptr(out), _stream(stream)))
+        return out
+
+    def decode(self, records, out=None, stream=None):
+        """Encoder::decode of OCTO records -> float32 [n, dim]."""
+        import torch
+        if not records.is_cuda:
+            raise ValueError("decode expects a CUDA tensor (there is no CPU path)")
+        records = records.contiguous()
+        n = records.numel() // self.record_bytes
+        if n * self.record_bytes != records.numel():
+            raise FormatError("code stream length mismatch")
+        if out is None:
+            out = torch.empty((n, self.cfg.dim), dtype=torch.float32, device=records.device)
+        _check(lib().oq_decode(self._h, _ptr(records), n, _ptr(out), _stream(stream)))
+        return out
+
+    def validate_records(self, records, stream=None):
+        """unpack_keys padding checks on device; raises FormatError."""
+        n = records.numel() // self.record_bytes
+        _check(lib().oq_validate_records(self._h, _ptr(records.contiguous()), n,
+                                         _stream(stream)))
+
+    # -- single-key convenience mirrors (host fp64 in, like the reference) -----
+    def encode(self, k):
+        """Encoder::encode(span<const double>) -> one OCTO record (bytes)."""
+        import torch
+        k = np.asarray(k, np.float64)
+        if k.shape != (self.cfg.dim,):
+            raise ValueError("key dimension mismatch")
+        t = torch.from_numpy(k.copy()).cuda().reshape(1, -1)
+        return bytes(self.compress(t).cpu().numpy().tobytes())
+
+    def tile_bytes(self, role):
+        return lib().oq_cache_tile_bytes(self._h, role)
+
+
+def pack_keys(cfg: CodecConfig, records):
+    """pack_keys (codec.hpp:364-396): 20-byte OCTO header + records."""
+    c = cfg._c()
+    rb = record_bytes(cfg)
+    if hasattr(records, "cpu"):
+        records = records.cpu().numpy()
+    records = np.ascontiguousarray(records, np.uint8).reshape(-1)
+    if records.size % rb:
+        raise ValueError("key shape does not match config")
+    hdr = C.create_string_buffer(20)
+    _check(lib().oq_wire_header(C.byref(c), records.size // rb, hdr))
+    return hdr.raw + records.tobytes()
+
+
+def unpack_keys(blob: bytes, device="cuda"):
+    """unpack_keys (codec.hpp:410-465) -> (CodecConfig, uint8 records tensor).
+
+    Header and payload size are checked on the host, padding bits on the GPU.
+    """
+    import torch
+    c = _Config()
+    cnt = C.c_uint64()
+    _check(lib().oq_wire_parse_header(blob, len(blob), C.byref(c), C.byref(cnt)))
+    cfg = CodecConfig(dim=c.dim, b_dir=c.b_dir, b_nrm=c.b_nrm, qjl=bool(c.qjl),
+                      qjl_seed=1 if c.qjl else 1)
+    rb = record_bytes(cfg)
+    recs = torch.frombuffer(bytearray(blob[20:]), dtype=torch.uint8).reshape(-1, rb) \
+        if cnt.value else torch.empty((0, rb), dtype=torch.uint8)
+    recs = recs.to(device)
+    if cnt.value:
+        enc = Encoder(cfg)
+        enc.validate_records(recs)
+    return cfg, recs
+
+
+class KVCache:
+    """Compressed K/V cache in the attention tile formats.
+
+    Streams are (batch, kv head) pairs; each holds ``cap_tokens`` tokens in
+    32-token tiles (K and V tile formats differ; see attention.cu).
+    """
+
+    def __init__(self, enc_k: Encoder, enc_v: Encoder, B, Hkv, cap_tokens, device="cuda"):
+        import torch
+        self.enc_k, self.enc_v = enc_k, enc_v
+        self.B, self.Hkv, self.cap = B, Hkv, int(cap_tokens)
+        kt, vt = enc_k.tile_bytes(ROLE_K), enc_v.tile_bytes(ROLE_V)
+        if kt == 0 or vt == 0:
+            raise NotImplementedError("attention tiles need dim 128 and 2*b_dir+b_nrm in {7,10}")
+        ntiles = (self.cap + 31) // 32
+        self.k = torch.zeros(B * Hkv * ntiles * kt, dtype=torch.uint8, device=device)
+        self.v = torch.zeros(B * Hkv * ntiles * vt, dtype=torch.uint8, device=device)
+        self.tokens = 0
+
+    def pack(self, k_records, v_records, n_tokens, rec_stride=None, stream=None):
+        """Fill from OCTO records [B*Hkv, rec_stride, rb] (first n_tokens each)."""
+        rs = rec_stride if rec_stride is not None else n_tokens
+        n = self.B * self.Hkv
+        _check(lib().oq_cache_pack(self.enc_k.handle, ROLE_K, _ptr(k_records), n, n_tokens, rs,
+                                   _ptr(self.k), self.cap, _stream(stream)))
+        _check(lib().oq_cache_pack(self.enc_v.handle, ROLE_V, _ptr(v_records), n, n_tokens, rs,
+                                   _ptr(self.v), self.cap, _stream(stream)))
+        self.tokens = n_tokens
+
+    def nbytes_per_token(self):
+        return (self.enc_k.tile_bytes(ROLE_K) + self.enc_v.tile_bytes(ROLE_V)) / 32.0
+
+
+def default_splits(B, Hkv, Hq, T, num_sms=148):
+    """Split-K count so that (B*Hkv*ceil(G/8)*splits) CTA work items fill the SMs evenly."""
+    hc = (Hq // Hkv + 7) // 8
+    streams = B * Hkv * hc
+    tiles = max(1, (T + 31) // 32)
+    best = 1
+    for waves in range(1, 64):
+        s = -(-waves * num_sms // streams)
+        if s <= tiles:
+            best = s
+            if (streams * s) % num_sms == 0 or waves >= 4:
+                break
+    return max(1, min(best, tiles))
+
+
+class _Workspace:
+    buf = {}
+
+    @classmethod
+    def get(cls, nbytes, device):
+        import torch
+        key = str(device)
+        b = cls.buf.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            cls.buf[key] = b
+        return b
+
+
+def _shape(cache: KVCache, Hq, T, seq_lens):
+    return _Shape(cache.B, Hq, cache.Hkv, T, cache.cap,
+                  seq_lens.data_ptr() if seq_lens is not None else None)
+
+
+def attention_decode(q, cache: KVCache, n_splits=None, seq_lens=None, T=None, out=None,
+                     stream=None):
+    """attention_decode (attention.hpp:50-73), batched GQA over compressed K and V.
+
+    q: CUDA float32 [B, Hq, dim].  Returns [B, Hq, dim] float32.
+    """
+    import torch
+    B, Hq, D = q.shape
+    T = cache.tokens if T is None else T
+    if n_splits is None:
+        n_splits = default_splits(B, cache.Hkv, Hq, T)
+    sh = _shape(cache, Hq, T, seq_lens)
+    L = lib()
+    ws_bytes = L.oq_attention_workspace_bytes(cache.enc_k.handle, cache.enc_v.handle,
+                                              C.byref(sh), n_splits)
+    ws = _Workspace.get(ws_bytes, q.device)
+    if out is None:
+        out = torch.empty((B, Hq, D), dtype=torch.float32, device=q.device)
+    q = q.contiguous().float()
+    _check(L.oq_attention_decode(cache.enc_k.handle, cache.enc_v.handle, C.byref(sh), _ptr(q),
+                                 _ptr(cache.k), _ptr(cache.v), _ptr(out), n_splits, _ptr(ws),
+                                 ws.numel(), _stream(stream)))
+    return out
+
+
+def attention_partials(q, cache: KVCache, t_begin, t_end, n_splits=None, T=None, seq_lens=None,
+                       out=None, stream=None):
+    """SoftmaxState of tokens [t_begin, t_end) per (b, q head): [B*Hq, 132] fp32."""
+    import torch
+    B, Hq, D = q.shape
+    T = cache.tokens if T is None else T
+    if n_splits is None:
+        n_splits = default_splits(B, cache.Hkv, Hq, max(1, t_end - t_begin))
+    sh = _shape(cache, Hq, T, seq_lens)
+    L = lib()
+    ws_bytes = L.oq_attention_workspace_bytes(cache.enc_k.handle, cache.enc_v.handle,
+                                              C.byref(sh), n_splits)
+    ws = _Workspace.get(ws_bytes, q.device)
+    if out is None:
+        out = torch.empty((B * Hq, 4 + D), dtype=torch.float32, device=q.device)
+    q = q.contiguous().float()
+    _check(L.oq_attention_partials(cache.enc_k.handle, cache.enc_v.handle, C.byref(sh), _ptr(q),
+                                   _ptr(cache.k), _ptr(cache.v), t_begin, t_end, _ptr(out),
+                                   n_splits, _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
+def attention_combine(enc_v: Encoder, partials, rows, n_parts, row_stride, part_stride,
+                      finalize=True, out=None, stream=None):
+    """Merge partials in token order (SoftmaxState::merge) and finalize."""
+    import torch
+    D = enc_v.cfg.dim
+    if out is None:
+        out = torch.empty((rows, D if finalize else 4 + D), dtype=torch.float32,
+                          device=partials.device)
+    _check(lib().oq_attention_combine(enc_v.handle, _ptr(partials), rows, n_parts, row_stride,
+                                      part_stride, 1 if finalize else 0, _ptr(out),
+                                      _stream(stream)))
+    return out

@@ -1,0 +1,811 @@
+// attention.cu — K3/K4/K5: fused split-K GQA decode attention over the
+// OCTOPUS-compressed KV cache on sm_100a (attention.hpp:50-73 semantics, V
+// compressed with the same codec and accumulated in its rotated frame).
+//
+// Per SM, one persistent CTA of 8 warps:
+//   * the joint dequant table T[code] = fp16 (rho x, rho y | rho z, 0),
+//     code = ixi | ieta << b_dir | irho << 2 b_dir, sits in shared memory
+//     replicated 16x so the 16 lanes of a half-warp always hit 16 distinct
+//     bank pairs (conflict-free LDS.64 for arbitrary codes);
+//   * each warp streams 32-token tiles of packed K and V codes from HBM into
+//     registers (coalesced; the next tile is prefetched while the current
+//     one is processed);
+//   * K codes dequantize straight into mma.sync A fragments of S^T = K_hat Q^T
+//     (M = 16 tokens, N = 8 query heads of the GQA group, K = 144 triplet-
+//     permuted dims; Q is permuted identically by the prep kernel);
+//   * online softmax in the log2 domain (q pre-scaled by log2(e)/sqrt(d));
+//     accumulator rescaling is skipped while no running max moves;
+//   * P^T becomes the PV B operand through movmatrix.trans, V codes
+//     dequantize into A fragments of V_hat^T (M = 144 permuted dims, K = 16
+//     tokens), so out^T accumulates in the rotated V frame and the inverse V
+//     rotation runs once per (b, head) in the combine kernel.
+// Tile formats (see oq_cache_pack): each lane's codes form one contiguous
+// run, so extraction is a static shift+mask (funnel shift across words)
+// folded into the table address: 2 ALU ops + 1 LDS per triplet.
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace oqd {
+
+constexpr int kTileTok = 32;
+constexpr int kNT = 43;  // triplets at dim 128
+constexpr int kAttnWarps = 8;
+constexpr int kPartW = 132;  // (m, l, 0, 0, acc[128]): acc 16-byte aligned
+
+// ---------------------------------------------------------------------------
+// Tile geometry, shared by the packer and the kernels.
+//
+// K tile (32 tokens): gamma[8][4] f32 ([g][k] = token g + 8k) | code area |
+//   [QJL: gamma_r[8][4] f16 | signs[8 g][4 c][4 k] u32 (word c of token g+8k)]
+//   code area: lane l = 4g + c owns triplets t = 11c + u (u < 11, 10 for
+//   c = 3) of tokens g + 8k (k < 4); code slot u*4 + k, W bits each,
+//   LSB-first, block padded to a word.
+// V tile: gamma[8][4] | code area: lane l owns triplets t = 6g + u (u < 6,
+//   1 for g = 7) of tokens v_token(c, k) (k < 8); slot u*8 + k.
+__host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+__host__ __device__ inline int kw_full(int W) { return cdiv(44 * W, 32); }
+__host__ __device__ inline int kw_3(int W) { return cdiv(40 * W, 32); }
+__host__ __device__ inline int vw_full(int W) { return cdiv(48 * W, 32); }
+__host__ __device__ inline int vw_7(int W) { return cdiv(8 * W, 32); }
+__host__ __device__ inline int kcode_words(int W) { return 8 * (3 * kw_full(W) + kw_3(W)); }
+__host__ __device__ inline int vcode_words(int W) { return 28 * vw_full(W) + 4 * vw_7(W); }
+__host__ __device__ inline int ktile_bytes(int W, int qjl) {
+  return (128 + 4 * kcode_words(W) + (qjl ? 64 + 512 : 0) + 15) & ~15;
+}
+__host__ __device__ inline int vtile_bytes(int W) { return (128 + 4 * vcode_words(W) + 15) & ~15; }
+__host__ __device__ inline int k_block_off(int W, int lane) {
+  const int g = lane >> 2, c = lane & 3;
+  return g * (3 * kw_full(W) + kw_3(W)) + c * kw_full(W);
+}
+__host__ __device__ inline int v_block_off(int W, int lane) {
+  const int g = lane >> 2, c = lane & 3;
+  return g < 7 ? lane * vw_full(W) : 28 * vw_full(W) + c * vw_7(W);
+}
+__host__ __device__ inline int k_token(int g, int k) { return g + 8 * k; }
+__host__ __device__ inline int v_token(int c, int k) {
+  return 16 * (k >> 2) + 2 * c + (k & 1) + 8 * ((k >> 1) & 1);
+}
+
+// K slot sigma (0..17) of lane c.  Blocks kb = (2kb, 2kb+1):
+//   kb0 (xy0, xy1) kb1 (xy2, xy3) kb2 (z01, z23) kb3 (xy4, xy5) kb4 (xy6, xy7)
+//   kb5 (z45, z67) kb6 (xy8, xy9) kb7 (xy10, z89) kb8 (z10, -)
+// Returns the two rotated-frame dims of the slot's fp16 pair (-1 = zero).
+__host__ __device__ inline void k_slot_dims(int c, int sigma, int& d0, int& d1) {
+  int kind = 3, u = 0;  // 0 xy(u), 1 z(u, u+1), 2 z(u), 3 none
+  if (sigma < 12) {
+    const int base = 4 * (sigma / 6), r = sigma % 6;
+    if (r < 4) { kind = 0; u = base + r; }
+    else { kind = 1; u = base + 2 * (r - 4); }
+  } else {
+    const int r = sigma - 12;
+    if (r < 3) { kind = 0; u = 8 + r; }
+    else if (r == 3) { kind = 1; u = 8; }
+    else if (r == 4) { kind = 2; u = 10; }
+  }
+  const int t = 11 * c + u;
+  d0 = d1 = -1;
+  if (kind == 0) { d0 = 3 * t; d1 = 3 * t + 1; }
+  else if (kind == 1) { d0 = 3 * t + 2; d1 = 3 * (t + 1) + 2; }
+  else if (kind == 2) { d0 = 3 * t + 2; }
+  if (d0 >= 128) d0 = -1;
+  if (d1 >= 128) d1 = -1;
+}
+
+// Rotated-frame dim behind V row-slot rho (0..17) of lane g; -1 = dummy row.
+__host__ __device__ inline int v_row_dim(int g, int rho) {
+  const int t = 6 * g + rho / 3, d = 3 * t + rho % 3;
+  return (t < kNT && d < 128) ? d : -1;
+}
+
+// ---------------------------------------------------------------------------
+template <int W, int N>
+__device__ __forceinline__ uint32_t code_addr(const uint32_t (&w)[N], int slot, uint32_t off) {
+  // byte offset = code * 128 + replica * 8; the table base is 2^(7+W)-aligned
+  // in the shared window, so the OR below is an ADD.
+  const int pos = slot * W, i = pos >> 5, sh = pos & 31;
+  constexpr uint32_t M7 = ((1u << W) - 1u) << 7;
+  uint32_t v;
+  if (sh + W <= 32) v = sh >= 7 ? (w[i] >> (sh - 7)) : (w[i] << (7 - sh));
+  else v = __funnelshift_r(w[i], w[i + 1], sh - 7);
+  return (v & M7) | off;
+}
+
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 r;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(addr));
+  return r;
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t movtrans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  const __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// +-1 fp16 pair from sign bits (sigma, sigma + 16) of ~w: bit 1 => +1.
+__device__ __forceinline__ uint32_t sign_pair(uint32_t nw, int sigma) {
+  return ((nw << (15 - sigma)) & 0x80008000u) | 0x3C003C00u;
+}
+
+// ---------------------------------------------------------------------------
+struct AttnKParams {
+  const uint2* tab;  // global joint table (2^W entries)
+  const uint8_t* kcache;
+  const uint8_t* vcache;
+  size_t k_tiles_cap, v_tiles_cap;
+  const uint32_t* qfrag;  // [streams*HC][32][QF]
+  float* partials;        // [B*Hq][n_parts][132]
+  const int32_t* seq_lens;
+  size_t T, t_begin, t_end;
+  int B, Hq, Hkv, G, HC;
+  int splits, n_parts, n_items;
+};
+
+template <int W, bool QJL>
+struct Cfg {
+  static constexpr int KWF = (44 * W + 31) / 32, KW3 = (40 * W + 31) / 32;
+  static constexpr int VWF = (48 * W + 31) / 32, VW7 = (8 * W + 31) / 32;
+  static constexpr int KCODE = 8 * (3 * KWF + KW3), VCODE = 28 * VWF + 4 * VW7;
+  static constexpr int KTILE = (128 + 4 * KCODE + (QJL ? 576 : 0) + 15) & ~15;
+  static constexpr int VTILE = (128 + 4 * VCODE + 15) & ~15;
+  static constexpr int QF = 18 + (QJL ? 16 : 0);
+  static constexpr int TAB_BYTES = (1 << W) * 16 * 8;
+  static constexpr int SMEM = TAB_BYTES + kAttnWarps * 8 * kPartW * 4;
+};
+
+template <int W, bool QJL>
+struct TileRegs {
+  uint32_t kc[Cfg<W, QJL>::KWF];
+  uint32_t vc[Cfg<W, QJL>::VWF];
+  float4 gk, gv;
+  uint2 gr;
+  uint4 sg;
+};
+
+template <int W, bool QJL>
+__device__ __forceinline__ void load_tile(TileRegs<W, QJL>& r, const AttnKParams& P,
+                                          size_t stream, size_t tile, int g, int c, int koff,
+                                          int voff) {
+  using C = Cfg<W, QJL>;
+  const uint8_t* kt = P.kcache + (stream * P.k_tiles_cap + tile) * (size_t)C::KTILE;
+  const uint8_t* vt = P.vcache + (stream * P.v_tiles_cap + tile) * (size_t)C::VTILE;
+  r.gk = __ldg(reinterpret_cast<const float4*>(kt) + g);
+  r.gv = __ldg(reinterpret_cast<const float4*>(vt) + g);
+  const uint32_t* kw = reinterpret_cast<const uint32_t*>(kt + 128) + koff;
+  const uint32_t* vw = reinterpret_cast<const uint32_t*>(vt + 128) + voff;
+  const int nk = c < 3 ? C::KWF : C::KW3, nv = g < 7 ? C::VWF : C::VW7;
+#pragma unroll
+  for (int i = 0; i < C::KWF; ++i) r.kc[i] = i < nk ? __ldg(kw + i) : 0u;
+#pragma unroll
+  for (int i = 0; i < C::VWF; ++i) r.vc[i] = i < nv ? __ldg(vw + i) : 0u;
+  if (QJL) {
+    const uint8_t* qa = kt + 128 + 4 * C::KCODE;
+    r.gr = __ldg(reinterpret_cast<const uint2*>(qa) + g);
+    r.sg = __ldg(reinterpret_cast<const uint4*>(qa + 64) + (4 * g + c));
+  }
+}
+
+// Online-softmax state of one warp for its 8 heads (2 per lane).
+struct WarpState {
+  float acc[9][4];
+  float m[2], l[2];
+};
+
+template <int W, bool QJL>
+__device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL>& R,
+                                             const uint32_t (&qf)[Cfg<W, QJL>::QF],
+                                             uint32_t toff, size_t tok0, size_t lo, size_t hi,
+                                             int g, int c) {
+  const float NEG_INF = -__int_as_float(0x7f800000);
+  float gk[4] = {R.gk.x, R.gk.y, R.gk.z, R.gk.w};
+  float gv[4] = {R.gv.x, R.gv.y, R.gv.z, R.gv.w};
+  bool ok[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const size_t t = tok0 + k_token(g, k);
+    ok[k] = t >= lo && t < hi;
+    if (!ok[k]) gk[k] = gv[k] = 0.f;
+  }
+
+  // ---- S^T = K_hat Q^T ----------------------------------------------------
+  float sc[4][2];  // [token slot k][head 2c + h2]
+#pragma unroll
+  for (int st = 0; st < 2; ++st) {
+    const int k0 = 2 * st, k1 = 2 * st + 1;  // rows g, g+8 of this sub-tile
+    float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int grp = 0; grp < 2; ++grp) {
+      uint2 a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        a[r] = lds64(code_addr<W>(R.kc, (4 * grp + r) * 4 + k0, toff));
+        b[r] = lds64(code_addr<W>(R.kc, (4 * grp + r) * 4 + k1, toff));
+      }
+      const int kb = 3 * grp;
+      mma16816(d, a[0].x, b[0].x, a[1].x, b[1].x, qf[2 * kb], qf[2 * kb + 1]);
+      mma16816(d, a[2].x, b[2].x, a[3].x, b[3].x, qf[2 * kb + 2], qf[2 * kb + 3]);
+      mma16816(d, __byte_perm(a[0].y, a[1].y, 0x5410), __byte_perm(b[0].y, b[1].y, 0x5410),
+               __byte_perm(a[2].y, a[3].y, 0x5410), __byte_perm(b[2].y, b[3].y, 0x5410),
+               qf[2 * kb + 4], qf[2 * kb + 5]);
+    }
+    {
+      uint2 a[3], b[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        a[r] = lds64(code_addr<W>(R.kc, (8 + r) * 4 + k0, toff));
+        b[r] = lds64(code_addr<W>(R.kc, (8 + r) * 4 + k1, toff));
+      }
+      mma16816(d, a[0].x, b[0].x, a[1].x, b[1].x, qf[12], qf[13]);
+      mma16816(d, a[2].x, b[2].x, __byte_perm(a[0].y, a[1].y, 0x5410),
+               __byte_perm(b[0].y, b[1].y, 0x5410), qf[14], qf[15]);
+      mma16816(d, a[2].y, b[2].y, 0u, 0u, qf[16], qf[17]);
+    }
+    if (QJL) {
+      // residual sketch: sum_i (+-1)_i q_sketch_i on the tensor cores
+      const uint32_t w0 = ~(st ? R.sg.z : R.sg.x), w1 = ~(st ? R.sg.w : R.sg.y);
+      float e[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kb = 0; kb < 8; ++kb)
+        mma16816(e, sign_pair(w0, 2 * kb), sign_pair(w1, 2 * kb), sign_pair(w0, 2 * kb + 1),
+                 sign_pair(w1, 2 * kb + 1), qf[18 + 2 * kb], qf[18 + 2 * kb + 1]);
+      const uint32_t grw = st ? R.gr.y : R.gr.x;
+      const float gr0 = __half2float(__ushort_as_half((unsigned short)(grw & 0xffff)));
+      const float gr1 = __half2float(__ushort_as_half((unsigned short)(grw >> 16)));
+      d[0] += gr0 * e[0];
+      d[1] += gr0 * e[1];
+      d[2] += gr1 * e[2];
+      d[3] += gr1 * e[3];
+    }
+    sc[k0][0] = ok[k0] ? d[0] * gk[k0] : NEG_INF;
+    sc[k0][1] = ok[k0] ? d[1] * gk[k0] : NEG_INF;
+    sc[k1][0] = ok[k1] ? d[2] * gk[k1] : NEG_INF;
+    sc[k1][1] = ok[k1] ? d[3] * gk[k1] : NEG_INF;
+  }
+
+  // ---- online softmax (log2 domain) ----------------------------------------
+  float mt[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float v = fmaxf(fmaxf(sc[0][h], sc[1][h]), fmaxf(sc[2][h], sc[3][h]));
+    v = fmaxf(v, __shfl_xor_sync(kFull, v, 4));
+    v = fmaxf(v, __shfl_xor_sync(kFull, v, 8));
+    v = fmaxf(v, __shfl_xor_sync(kFull, v, 16));
+    mt[h] = fmaxf(v, S.m[h]);
+  }
+  if (__any_sync(kFull, mt[0] > S.m[0] || mt[1] > S.m[1])) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float f = S.m[h] == NEG_INF ? 1.f : ex2(S.m[h] - mt[h]);
+      S.l[h] *= f;
+#pragma unroll
+      for (int mb = 0; mb < 9; ++mb) {
+        S.acc[mb][h] *= f;
+        S.acc[mb][2 + h] *= f;
+      }
+      S.m[h] = mt[h];
+    }
+  }
+  float p[4][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float mref = S.m[h] == NEG_INF ? 0.f : S.m[h];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p[k][h] = ex2(sc[k][h] - mref);
+    S.l[h] += (p[0][h] + p[1][h]) + (p[2][h] + p[3][h]);
+  }
+  uint32_t pb[2][2];  // PV B fragments per 16-token sub-tile
+#pragma unroll
+  for (int st = 0; st < 2; ++st) {
+    pb[st][0] = movtrans(pack_h2(p[2 * st][0] * gv[2 * st], p[2 * st][1] * gv[2 * st]));
+    pb[st][1] = movtrans(pack_h2(p[2 * st + 1][0] * gv[2 * st + 1], p[2 * st + 1][1] * gv[2 * st + 1]));
+  }
+
+  // ---- out^T += V_hat^T P^T ------------------------------------------------
+#pragma unroll
+  for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+    for (int grp = 0; grp < 3; ++grp) {
+      uint2 e[2][4];
+#pragma unroll
+      for (int uu = 0; uu < 2; ++uu)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          e[uu][q] = lds64(code_addr<W>(R.vc, (2 * grp + uu) * 8 + 4 * kk + q, toff));
+#pragma unroll
+      for (int mbl = 0; mbl < 3; ++mbl) {
+        uint32_t a[4];
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const int rho = 2 * mbl + half, uu = rho / 3, j = rho % 3;
+#pragma unroll
+          for (int pr = 0; pr < 2; ++pr) {  // token pair A (q 0,1) / B (q 2,3)
+            const uint2 x0 = e[uu][2 * pr], x1 = e[uu][2 * pr + 1];
+            uint32_t v;
+            if (j == 0) v = __byte_perm(x0.x, x1.x, 0x5410);
+            else if (j == 1) v = __byte_perm(x0.x, x1.x, 0x7632);
+            else v = __byte_perm(x0.y, x1.y, 0x5410);
+            a[2 * pr + half] = v;
+          }
+        }
+        mma16816(S.acc[3 * grp + mbl], a[0], a[1], a[2], a[3], pb[kk][0], pb[kk][1]);
+      }
+    }
+  }
+}
+
+template <int W, bool QJL>
+__global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const AttnKParams P) {
+  using C = Cfg<W, QJL>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint2* tab = reinterpret_cast<uint2*>(smem);
+  float* merge = reinterpret_cast<float*>(smem + C::TAB_BYTES);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, c = lane & 3;
+
+  for (int i = tid; i < (1 << W) * 16; i += blockDim.x) tab[i] = P.tab[i >> 4];
+  const uint32_t tbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
+  if (tbase & ((1u << (7 + W)) - 1u)) __trap();  // the OR-addressing needs an aligned table
+  const uint32_t toff = tbase | ((lane & 15) << 3);
+  const int koff = k_block_off(W, lane), voff = v_block_off(W, lane);
+  const float NEG_INF = -__int_as_float(0x7f800000);
+  __syncthreads();
+
+  for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+    const int split = item % P.splits;
+    const int sh = item / P.splits;  // stream * HC + hc
+    const int hc = sh % P.HC;
+    const size_t stream = sh / P.HC;
+    const int b = (int)(stream / P.Hkv), kvh = (int)(stream % P.Hkv);
+
+    uint32_t qf[C::QF];
+    {
+      const uint32_t* src = P.qfrag + ((size_t)sh * 32 + lane) * C::QF;
+#pragma unroll
+      for (int i = 0; i < C::QF; ++i) qf[i] = __ldg(src + i);
+    }
+    size_t len = P.T;
+    if (P.seq_lens) len = min((size_t)max(P.seq_lens[b], 0), P.T);
+    const size_t lo = P.t_begin, hi = min(P.t_end, len);
+    size_t tlo = 0, thi = 0;
+    if (hi > lo) {
+      const size_t a = lo / kTileTok, z = (hi + kTileTok - 1) / kTileTok;
+      tlo = a + (z - a) * split / P.splits;
+      thi = a + (z - a) * (split + 1) / P.splits;
+    }
+
+    WarpState S;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) S.acc[i][0] = S.acc[i][1] = S.acc[i][2] = S.acc[i][3] = 0.f;
+    S.m[0] = S.m[1] = NEG_INF;
+    S.l[0] = S.l[1] = 0.f;
+
+    TileRegs<W, QJL> ra, rb;
+    size_t tile = tlo + warp;
+    if (tile < thi) load_tile<W, QJL>(ra, P, stream, tile, g, c, koff, voff);
+    while (tile < thi) {
+      size_t tn = tile + kAttnWarps;
+      if (tn < thi) load_tile<W, QJL>(rb, P, stream, tn, g, c, koff, voff);
+      process_tile<W, QJL>(S, ra, qf, toff, tile * kTileTok, lo, hi, g, c);
+      tile = tn;
+      if (tile >= thi) break;
+      tn = tile + kAttnWarps;
+      if (tn < thi) load_tile<W, QJL>(ra, P, stream, tn, g, c, koff, voff);
+      process_tile<W, QJL>(S, rb, qf, toff, tile * kTileTok, lo, hi, g, c);
+      tile = tn;
+    }
+
+    // ---- per-warp reduction of l over the 8 row groups ----------------------
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float v = S.l[h];
+      v += __shfl_xor_sync(kFull, v, 4);
+      v += __shfl_xor_sync(kFull, v, 8);
+      v += __shfl_xor_sync(kFull, v, 16);
+      S.l[h] = v;
+    }
+    float* mw = merge + warp * 8 * kPartW;
+    if (g == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        mw[(2 * c + h) * kPartW + 0] = S.m[h];
+        mw[(2 * c + h) * kPartW + 1] = S.l[h];
+      }
+    }
+#pragma unroll
+    for (int mb = 0; mb < 9; ++mb)
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int d = v_row_dim(g, 2 * mb + half);
+        if (d >= 0) {
+          mw[(2 * c) * kPartW + 4 + d] = S.acc[mb][2 * half];
+          mw[(2 * c + 1) * kPartW + 4 + d] = S.acc[mb][2 * half + 1];
+        }
+      }
+    __syncthreads();
+    // ---- merge the 8 warps (SoftmaxState::merge, attention.hpp:36-44) -------
+    const int nh = min(8, P.G - 8 * hc);
+    for (int idx = tid; idx < nh * kPartW; idx += blockDim.x) {
+      const int h = idx / kPartW, j = idx % kPartW;
+      float M = NEG_INF;
+#pragma unroll
+      for (int w = 0; w < kAttnWarps; ++w) {
+        const float* mm = merge + (w * 8 + h) * kPartW;
+        if (mm[1] > 0.f) M = fmaxf(M, mm[0]);
+      }
+      float v = 0.f;
+      if (j == 0) {
+        v = M;
+      } else if (j == 2 || j == 3) {
+        v = 0.f;
+      } else {
+#pragma unroll
+        for (int w = 0; w < kAttnWarps; ++w) {
+          const float* mm = merge + (w * 8 + h) * kPartW;
+          if (mm[1] > 0.f) v += mm[j] * ex2(mm[0] - M);
+        }
+      }
+      const size_t row = (size_t)b * P.Hq + (size_t)kvh * P.G + 8 * hc + h;
+      P.partials[(row * P.n_parts + split) * kPartW + j] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: query prep (Encoder::prepare, codec.hpp:282-292) -> mma B fragments.
+// q_rot = R_k q scaled by log2(e)/sqrt(d); QJL: q_sketch = R' q_rot with the
+// estimator constant sqrt(pi/(2d)) (qjl.hpp:47) folded in.
+struct QPrepParams {
+  const float* q;
+  uint32_t* qfrag;
+  int Hq, Hkv, G, HC, QF;
+  uint32_t smask[4], qmask[4];
+  float inv_sqrt_d;
+  int qjl;
+};
+
+__device__ __forceinline__ void wht128_lane4(float (&y)[4], int lane) {
+  // normalized-free WHT over 128 values, 4 consecutive per lane
+  {
+    const float a = y[0], b = y[1], c2 = y[2], d = y[3];
+    y[0] = a + b; y[1] = a - b; y[2] = c2 + d; y[3] = c2 - d;
+    const float e0 = y[0], e1 = y[1];
+    y[0] = e0 + y[2]; y[1] = e1 + y[3]; y[2] = e0 - y[2]; y[3] = e1 - y[3];
+  }
+#pragma unroll
+  for (int lm = 1; lm < 32; lm <<= 1) {
+    const bool up = lane & lm;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float o = __shfl_xor_sync(kFull, y[i], lm);
+      y[i] = up ? o - y[i] : y[i] + o;
+    }
+  }
+}
+
+__global__ void qprep_kernel(QPrepParams P) {
+  __shared__ float qs[8][129];
+  __shared__ float qk[8][129];
+  const int sh = blockIdx.x, hc = sh % P.HC, stream = sh / P.HC;
+  const int b = stream / P.Hkv, kvh = stream % P.Hkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = 8 * hc + warp;
+  const float log2e = 1.4426950408889634f;
+  if (h < P.G) {
+    const float* q = P.q + ((size_t)b * P.Hq + (size_t)kvh * P.G + h) * 128;
+    float y[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = 4 * lane + i;
+      const float v = q[e];
+      y[i] = ((P.smask[e >> 5] >> (e & 31)) & 1u) ? -v : v;
+    }
+    wht128_lane4(y, lane);
+    const float s_attn = P.inv_sqrt_d * P.inv_sqrt_d * log2e;  // rotation norm x 1/sqrt(d) x log2e
+#pragma unroll
+    for (int i = 0; i < 4; ++i) qs[warp][4 * lane + i] = y[i] * s_attn;
+    if (P.qjl) {
+      float z[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = 4 * lane + i;
+        const float v = y[i] * P.inv_sqrt_d;  // q_rot
+        z[i] = ((P.qmask[e >> 5] >> (e & 31)) & 1u) ? -v : v;
+      }
+      wht128_lane4(z, lane);
+      const float s_sk = P.inv_sqrt_d * P.inv_sqrt_d * log2e * sqrtf(1.5707963267948966f / 128.f);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) qk[warp][4 * lane + i] = z[i] * s_sk;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) qs[warp][4 * lane + i] = qk[warp][4 * lane + i] = 0.f;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int g = lane >> 2, c = lane & 3;
+    uint32_t* dst = P.qfrag + ((size_t)sh * 32 + lane) * P.QF;
+    for (int sigma = 0; sigma < 18; ++sigma) {
+      int d0, d1;
+      k_slot_dims(c, sigma, d0, d1);
+      dst[sigma] = pack_h2(d0 >= 0 ? qs[g][d0] : 0.f, d1 >= 0 ? qs[g][d1] : 0.f);
+    }
+    if (P.qjl)
+      for (int sigma = 0; sigma < 16; ++sigma)
+        dst[18 + sigma] = pack_h2(qk[g][32 * c + sigma], qk[g][32 * c + sigma + 16]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: merge partials in order, then acc/l and the inverse V rotation.
+struct CombineParams {
+  const float* parts;
+  float* out;
+  int rows, n_parts, finalize;
+  size_t row_stride, part_stride;
+  uint32_t smask[4];
+  float inv_sqrt_d;
+};
+
+__global__ void combine_kernel(CombineParams P) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= P.rows) return;
+  const float NEG_INF = -__int_as_float(0x7f800000);
+  const float* base = P.parts + (size_t)row * P.row_stride;
+  float M = NEG_INF;
+  for (int i = 0; i < P.n_parts; ++i) {
+    const float* pp = base + (size_t)i * P.part_stride;
+    if (pp[1] > 0.f) M = fmaxf(M, pp[0]);
+  }
+  float L = 0.f, y[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < P.n_parts; ++i) {
+    const float* pp = base + (size_t)i * P.part_stride;
+    if (pp[1] > 0.f) {
+      const float f = ex2(pp[0] - M);
+      L += pp[1] * f;
+      const float4 a = *reinterpret_cast<const float4*>(pp + 4 + 4 * lane);
+      y[0] += a.x * f; y[1] += a.y * f; y[2] += a.z * f; y[3] += a.w * f;
+    }
+  }
+  if (!P.finalize) {
+    float* o = P.out + (size_t)row * kPartW;
+    if (lane == 0) { o[0] = M; o[1] = L; o[2] = 0.f; o[3] = 0.f; }
+    *reinterpret_cast<float4*>(o + 4 + 4 * lane) = make_float4(y[0], y[1], y[2], y[3]);
+    return;
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) y[i] *= inv;
+  wht128_lane4(y, lane);
+  float* o = P.out + (size_t)row * 128;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int e = 4 * lane + i;
+    const float v = y[i] * P.inv_sqrt_d;
+    o[e] = ((P.smask[e >> 5] >> (e & 31)) & 1u) ? -v : v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// records -> attention tiles (oq_cache_pack).  One warp per (stream, tile).
+__device__ __forceinline__ uint32_t rec_joint(const OqCodecParams& p, const uint8_t* r, int t) {
+  if (t >= kNT) return 0u;
+  const uint32_t a = read_bits_safe(r + 4, 2 * t * p.b_dir, p.b_dir);
+  const uint32_t b = read_bits_safe(r + 4, (2 * t + 1) * p.b_dir, p.b_dir);
+  const uint32_t n = read_bits_safe(r + 4 + p.dir_bytes, t * p.b_nrm, p.b_nrm);
+  return a | (b << p.b_dir) | (n << (2 * p.b_dir));
+}
+
+__global__ void pack_tiles_kernel(OqCodecParams p, int role, const uint8_t* __restrict__ recs,
+                                  size_t n_streams, size_t n_tok, size_t rec_stride,
+                                  uint8_t* __restrict__ tiles, size_t tiles_cap) {
+  const int W = 2 * p.b_dir + p.b_nrm;
+  const int lane = threadIdx.x & 31;
+  const size_t wid = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  const size_t ntiles = (n_tok + 31) / 32;
+  if (wid >= n_streams * ntiles) return;
+  const size_t s = wid / ntiles, tile = wid % ntiles;
+  const int tb = role == 0 ? ktile_bytes(W, p.qjl) : vtile_bytes(W);
+  uint8_t* out = tiles + (s * tiles_cap + tile) * (size_t)tb;
+  const int g = lane >> 2, c = lane & 3;
+  auto rec = [&](int tt) -> const uint8_t* {
+    const size_t tok = tile * 32 + tt;
+    return tok < n_tok ? recs + (s * rec_stride + tok) * p.rec_bytes : nullptr;
+  };
+  auto gamma_of = [&](const uint8_t* r) -> float {
+    if (!r) return 0.f;
+    const uint32_t b = (uint32_t)r[0] | ((uint32_t)r[1] << 8) | ((uint32_t)r[2] << 16) |
+                       ((uint32_t)r[3] << 24);
+    return __uint_as_float(b);
+  };
+  if (lane < 8)
+    for (int k = 0; k < 4; ++k)
+      reinterpret_cast<float*>(out)[lane * 4 + k] = gamma_of(rec(k_token(lane, k)));
+  uint32_t* codes = reinterpret_cast<uint32_t*>(out + 128);
+  // build this lane's code run
+  uint32_t acc = 0;
+  int nbits = 0, wi = 0;
+  uint32_t* dst;
+  int nslots;
+  if (role == 0) {
+    dst = codes + k_block_off(W, lane);
+    nslots = (c < 3 ? 11 : 10) * 4;
+  } else {
+    dst = codes + v_block_off(W, lane);
+    nslots = (g < 7 ? 6 : 1) * 8;
+  }
+  for (int slot = 0; slot < nslots; ++slot) {
+    uint32_t code;
+    if (role == 0) {
+      const int u = slot >> 2, k = slot & 3;
+      const uint8_t* r = rec(k_token(g, k));
+      code = r ? rec_joint(p, r, 11 * c + u) : 0u;
+    } else {
+      const int u = slot >> 3, k = slot & 7;
+      const uint8_t* r = rec(v_token(c, k));
+      code = r ? rec_joint(p, r, 6 * g + u) : 0u;
+    }
+    // append W bits LSB-first
+    acc |= code << nbits;
+    nbits += W;
+    if (nbits >= 32) {
+      dst[wi++] = acc;
+      nbits -= 32;
+      acc = nbits ? code >> (W - nbits) : 0u;
+    }
+  }
+  if (nbits) dst[wi++] = acc;
+  if (role == 0 && p.qjl) {
+    uint8_t* qa = out + 128 + 4 * kcode_words(W);
+    const int sign_off = 4 + p.dir_bytes + p.nrm_bytes + 2;
+    if (lane < 8)
+      for (int k = 0; k < 4; ++k) {
+        const uint8_t* r = rec(k_token(lane, k));
+        const uint16_t grb = r ? (uint16_t)(r[sign_off - 2] | (r[sign_off - 1] << 8)) : 0;
+        reinterpret_cast<uint16_t*>(qa)[lane * 4 + k] = grb;
+      }
+    uint32_t* sg = reinterpret_cast<uint32_t*>(qa + 64) + (4 * g + c) * 4;
+    for (int k = 0; k < 4; ++k) {
+      const uint8_t* r = rec(k_token(g, k));
+      uint32_t w = 0;
+      if (r)
+        for (int i = 0; i < 4; ++i) w |= (uint32_t)r[sign_off + 4 * c + i] << (8 * i);
+      sg[k] = w;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+size_t attention_tile_bytes(const OqCodecParams& p, int role) {
+  const int W = 2 * p.b_dir + p.b_nrm;
+  if (p.dim != 128 || W > 13 || W < 3) return 0;
+  return role == 0 ? ktile_bytes(W, p.qjl) : vtile_bytes(W);
+}
+
+size_t attention_qfrag_bytes(const OqCodecParams& pk) {
+  return 32 * (18 + (pk.qjl ? 16 : 0)) * 4;
+}
+
+bool attention_fast_path_ok(const OqCodecParams& pk, const OqCodecParams& pv) {
+  const int W = 2 * pk.b_dir + pk.b_nrm;
+  return pk.dim == 128 && pv.dim == 128 && pk.b_dir == pv.b_dir && pk.b_nrm == pv.b_nrm &&
+         (W == 7 || W == 10) && !pv.qjl;
+}
+
+cudaError_t launch_pack_tiles(const OqCodecParams& p, int role, const uint8_t* recs,
+                              size_t n_streams, size_t n_tokens, size_t rec_stride,
+                              uint8_t* tiles, size_t tiles_cap, cudaStream_t st) {
+  const size_t warps = n_streams * ((n_tokens + 31) / 32);
+  if (warps == 0) return cudaSuccess;
+  const size_t blocks = (warps * 32 + 255) / 256;
+  pack_tiles_kernel<<<(unsigned)blocks, 256, 0, st>>>(p, role, recs, n_streams, n_tokens,
+                                                      rec_stride, tiles, tiles_cap);
+  return cudaGetLastError();
+}
+
+template <int W, bool QJL>
+static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int splits,
+                                 int G, int HC, cudaStream_t st, int num_sms) {
+  using C = Cfg<W, QJL>;
+  AttnKParams P;
+  P.tab = pk.joint16;
+  P.kcache = a.kcache;
+  P.vcache = a.vcache;
+  P.k_tiles_cap = a.k_tiles_cap;
+  P.v_tiles_cap = a.v_tiles_cap;
+  P.qfrag = static_cast<const uint32_t*>(a.qfrag);
+  P.partials = a.partials;
+  P.seq_lens = a.seq_lens;
+  P.T = a.T;
+  P.t_begin = a.t_begin;
+  P.t_end = a.t_end;
+  P.B = a.B;
+  P.Hq = a.Hq;
+  P.Hkv = a.Hkv;
+  P.G = G;
+  P.HC = HC;
+  P.splits = splits;
+  P.n_parts = a.n_parts;
+  P.n_items = a.B * a.Hkv * HC * splits;
+  cudaError_t e = cudaFuncSetAttribute(attn_partials_kernel<W, QJL>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (e != cudaSuccess) return e;
+  const int grid = P.n_items < num_sms ? P.n_items : num_sms;
+  attn_partials_kernel<W, QJL><<<grid, kAttnWarps * 32, C::SMEM, st>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecParams& pv,
+                                      const AttnArgs& a, int splits, cudaStream_t st,
+                                      int num_sms) {
+  const int G = a.Hq / a.Hkv, HC = (G + 7) / 8;
+  QPrepParams qp;
+  qp.q = a.q;
+  qp.qfrag = static_cast<uint32_t*>(a.qfrag);
+  qp.Hq = a.Hq;
+  qp.Hkv = a.Hkv;
+  qp.G = G;
+  qp.HC = HC;
+  qp.QF = 18 + (pk.qjl ? 16 : 0);
+  for (int i = 0; i < 4; ++i) {
+    qp.smask[i] = pk.sign_mask[i];
+    qp.qmask[i] = pk.qsign_mask[i];
+  }
+  qp.inv_sqrt_d = (float)pk.inv_sqrt_d;
+  qp.qjl = pk.qjl;
+  qprep_kernel<<<a.B * a.Hkv * HC, 256, 0, st>>>(qp);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int W = 2 * pk.b_dir + pk.b_nrm;
+  if (W == 10 && !pk.qjl) return launch_attn_t<10, false>(pk, a, splits, G, HC, st, num_sms);
+  if (W == 10 && pk.qjl) return launch_attn_t<10, true>(pk, a, splits, G, HC, st, num_sms);
+  if (W == 7 && !pk.qjl) return launch_attn_t<7, false>(pk, a, splits, G, HC, st, num_sms);
+  if (W == 7 && pk.qjl) return launch_attn_t<7, true>(pk, a, splits, G, HC, st, num_sms);
+  (void)pv;
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_attention_combine(const OqCodecParams& pv, const float* partials, int rows,
+                                     int n_parts, size_t row_stride, size_t part_stride,
+                                     int finalize, float* out, cudaStream_t st) {
+  CombineParams P;
+  P.parts = partials;
+  P.out = out;
+  P.rows = rows;
+  P.n_parts = n_parts;
+  P.finalize = finalize;
+  P.row_stride = row_stride;
+  P.part_stride = part_stride;
+  for (int i = 0; i < 4; ++i) P.smask[i] = pv.sign_mask[i];
+  P.inv_sqrt_d = (float)pv.inv_sqrt_d;
+  const int per_block = 4;
+  combine_kernel<<<(rows + per_block - 1) / per_block, 32 * per_block, 0, st>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace oqd

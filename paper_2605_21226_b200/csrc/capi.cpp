@@ -1,0 +1,499 @@
+// capi.cpp — the oq_* C ABI (include/octoquant_b200.h): argument validation
+// with the reference's error semantics, codec construction (host books ->
+// device tables) and kernel dispatch.  No CPU compute path exists here: every
+// data-path entry point launches an sm_100a kernel.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/octoquant_b200.h"
+#include "books.hpp"
+#include "codec_params.h"
+#include "kernels.h"
+
+struct oq_codec {
+  oq_config cfg;
+  OqCodecParams p;
+  int device = 0;
+  int num_sms = 148;
+  std::vector<void*> allocs;
+  std::vector<double> xi_c, rho_c;  // host copies (centroids)
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+oq_status fail(oq_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+struct FormatErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+bool is_pow2(uint32_t v) { return v && !(v & (v - 1)); }
+
+size_t rec_bytes(const oq_config& c) {
+  const size_t nt = (c.dim + 2) / 3;
+  return 4 + (2 * nt * c.b_dir + 7) / 8 + (nt * c.b_nrm + 7) / 8 +
+         (c.qjl ? 2 + (c.dim + 7) / 8 : 0);
+}
+
+oq_status validate(const oq_config* c) {
+  if (!c) return fail(OQ_ERR_INVALID_ARGUMENT, "null config");
+  if (!is_pow2(c->dim) || c->dim < 4)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "codec dim must be a power of two, >= 4");
+  if (c->b_dir < 1 || c->b_dir > 8 || c->b_nrm < 1 || c->b_nrm > 8)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "codec bits must be in [1,8]");
+  if (c->qjl && c->qjl_seed == c->rotation_seed)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "qjl_seed must differ from rotation_seed");
+  if (c->rounding > 3) return fail(OQ_ERR_INVALID_ARGUMENT, "unknown rounding mode");
+  return OQ_OK;
+}
+
+oq_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(OQ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename T>
+oq_status upload(oq_codec* c, const std::vector<T>& h, const T** out) {
+  void* d = nullptr;
+  const size_t bytes = std::max<size_t>(h.size() * sizeof(T), 16);
+  cudaError_t e = cudaMalloc(&d, bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  c->allocs.push_back(d);
+  if (!h.empty()) {
+    e = cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy");
+  }
+  *out = static_cast<const T*>(d);
+  return OQ_OK;
+}
+
+uint16_t half_bits(double v) {
+  const __half h = __double2half(v);
+  uint16_t b;
+  std::memcpy(&b, &h, 2);
+  return b;
+}
+
+oq_status build_codec(const oq_config* cfg, const oqh::Book& xi, const oqh::Book& rho,
+                      oq_codec** out) {
+  if (!out) return fail(OQ_ERR_INVALID_ARGUMENT, "null output handle");
+  if (cfg->dim > 256) return fail(OQ_ERR_UNSUPPORTED, "dim > 256 is not supported on device");
+  int dev = 0, nsm = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "no CUDA device (there is no CPU fallback)");
+  e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  auto* c = new oq_codec();
+  c->cfg = *cfg;
+  c->device = dev;
+  c->num_sms = nsm;
+  c->xi_c = xi.centroids;
+  c->rho_c = rho.centroids;
+  OqCodecParams& p = c->p;
+  std::memset(&p, 0, sizeof(p));
+  p.dim = cfg->dim;
+  p.nt = (cfg->dim + 2) / 3;
+  p.b_dir = cfg->b_dir;
+  p.b_nrm = cfg->b_nrm;
+  p.K = 1u << cfg->b_dir;
+  p.KR = 1u << cfg->b_nrm;
+  p.rounding = cfg->rounding;
+  p.qjl = cfg->qjl;
+  p.rec_bytes = (uint32_t)rec_bytes(*cfg);
+  p.dir_bytes = (2 * p.nt * p.b_dir + 7) / 8;
+  p.nrm_bytes = (p.nt * p.b_nrm + 7) / 8;
+  p.inv_sqrt_d = 1.0 / std::sqrt(static_cast<double>(cfg->dim));  // rotation.hpp:29
+  for (uint32_t i = 0; i < cfg->dim; ++i) {
+    if (oqh::rotation_sign_mask_word(cfg->rotation_seed, i)) p.sign_mask[i >> 5] |= 1u << (i & 31);
+    if (oqh::rotation_sign_mask_word(cfg->qjl_seed, i)) p.qsign_mask[i >> 5] |= 1u << (i & 31);
+  }
+  // Direction table: oct_decode of every centroid pair (codec.hpp:100-107).
+  const uint32_t K = p.K, KR = p.KR;
+  std::vector<double> dirs64(size_t(K) * K * 3);
+  std::vector<float> dirs32(size_t(K) * K * 4);
+  for (uint32_t a = 0; a < K; ++a)
+    for (uint32_t b = 0; b < K; ++b) {
+      const auto n = oqh::oct_decode(xi.centroids[a], xi.centroids[b]);
+      for (int j = 0; j < 3; ++j) {
+        dirs64[3 * (a * K + b) + j] = n[j];
+        dirs32[4 * (a * K + b) + j] = static_cast<float>(n[j]);
+      }
+      dirs32[4 * (a * K + b) + 3] = 0.f;
+    }
+  std::vector<float> rho32(KR);
+  for (uint32_t i = 0; i < KR; ++i) rho32[i] = static_cast<float>(rho.centroids[i]);
+  // Joint dequant table indexed by ixi | ieta << b_dir | irho << 2 b_dir:
+  // fp16 (rho x, rho y | rho z, 0), the attention kernel's lookup.
+  std::vector<uint2> joint;
+  const uint32_t W = 2 * p.b_dir + p.b_nrm;
+  if (W <= 16) {
+    joint.resize(size_t(1) << W);
+    for (uint32_t code = 0; code < (1u << W); ++code) {
+      const uint32_t a = code & (K - 1), b = (code >> p.b_dir) & (K - 1), r = code >> (2 * p.b_dir);
+      const double* n = &dirs64[3 * (a * K + b)];
+      const double rh = rho.centroids[r];
+      joint[code].x = half_bits(rh * n[0]) | (uint32_t(half_bits(rh * n[1])) << 16);
+      joint[code].y = half_bits(rh * n[2]);
+    }
+  }
+  oq_status s;
+  if ((s = upload(c, xi.boundaries, &p.xi_bnd)) || (s = upload(c, rho.boundaries, &p.rho_bnd)) ||
+      (s = upload(c, rho.centroids, &p.rho_c)) || (s = upload(c, dirs64, &p.dirs64)) ||
+      (s = upload(c, dirs32, &p.dirs32)) || (s = upload(c, rho32, &p.rho32)) ||
+      (s = upload(c, joint, &p.joint16))) {
+    oq_codec_destroy(c);
+    return s;
+  }
+  *out = c;
+  return OQ_OK;
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+oq_status check_codec(const oq_codec* c) {
+  if (!c) return fail(OQ_ERR_INVALID_ARGUMENT, "null codec");
+  int dev = -1;
+  cudaGetDevice(&dev);
+  if (dev != c->device) return fail(OQ_ERR_INVALID_ARGUMENT, "codec belongs to another device");
+  return OQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* oq_last_error(void) { return g_err.c_str(); }
+const char* oq_version(void) { return "octoquant-b200 0.1 (sm_100a)"; }
+
+oq_status oq_config_default(oq_config* cfg) {
+  if (!cfg) return fail(OQ_ERR_INVALID_ARGUMENT, "null config");
+  *cfg = oq_config{128, 3, 1, OQ_ROUND_LOCAL3X3, 0, 0, 1};
+  return OQ_OK;
+}
+
+oq_status oq_config_validate(const oq_config* cfg) { return validate(cfg); }
+
+oq_status oq_default_bit_split(int b, int* b_dir, int* b_nrm) {
+  if (b < 2) return fail(OQ_ERR_INVALID_ARGUMENT, "default bit split needs b >= 2");
+  if (b_dir) *b_dir = b + 1;
+  if (b_nrm) *b_nrm = b - 1;
+  return OQ_OK;
+}
+
+oq_status oq_parse_rounding(const char* name, int* r) {
+  static const char* names[] = {"scalar", "local2x2", "local3x3", "full"};
+  for (int i = 0; i < 4; ++i)
+    if (name && std::strcmp(name, names[i]) == 0) {
+      if (r) *r = i;
+      return OQ_OK;
+    }
+  return fail(OQ_ERR_INVALID_ARGUMENT,
+              std::string("unknown rounding mode: ") + (name ? name : "(null)"));
+}
+
+const char* oq_rounding_name(int r) {
+  switch (r) {
+    case 0: return "scalar";
+    case 1: return "local2x2";
+    case 2: return "local3x3";
+    case 3: return "full";
+  }
+  return "?";
+}
+
+double oq_effective_bits_per_coord(const oq_config* cfg) {
+  const double nt = (cfg->dim + 2) / 3;
+  double bits = 2.0 * nt * cfg->b_dir + nt * cfg->b_nrm + 32.0;
+  if (cfg->qjl) bits += cfg->dim + 16.0;
+  return bits / cfg->dim;
+}
+
+size_t oq_record_bytes(const oq_config* cfg) { return cfg ? rec_bytes(*cfg) : 0; }
+
+oq_status oq_xi_book(int bits, double* c, double* b) {
+  try {
+    const oqh::Book& bk = oqh::xi_book(bits);
+    if (c) std::memcpy(c, bk.centroids.data(), bk.centroids.size() * 8);
+    if (b) std::memcpy(b, bk.boundaries.data(), bk.boundaries.size() * 8);
+    return OQ_OK;
+  } catch (const std::exception& ex) {
+    return fail(OQ_ERR_INVALID_ARGUMENT, ex.what());
+  }
+}
+
+oq_status oq_rho_book(uint32_t dim, int bits, double* c, double* b) {
+  try {
+    const oqh::Book& bk = oqh::rho_book(dim, bits);
+    if (c) std::memcpy(c, bk.centroids.data(), bk.centroids.size() * 8);
+    if (b) std::memcpy(b, bk.boundaries.data(), bk.boundaries.size() * 8);
+    return OQ_OK;
+  } catch (const std::exception& ex) {
+    return fail(OQ_ERR_INVALID_ARGUMENT, ex.what());
+  }
+}
+
+oq_status oq_codec_create(const oq_config* cfg, oq_codec** out) {
+  oq_status s = validate(cfg);
+  if (s) return s;
+  try {
+    return build_codec(cfg, oqh::xi_book(cfg->b_dir), oqh::rho_book(cfg->dim, cfg->b_nrm), out);
+  } catch (const std::exception& ex) {
+    return fail(OQ_ERR_INVALID_ARGUMENT, ex.what());
+  }
+}
+
+oq_status oq_codec_create_custom(const oq_config* cfg, const double* xc, int xbits,
+                                 const double* rc, int rbits, oq_codec** out) {
+  oq_status s = validate(cfg);
+  if (s) return s;
+  if (!xc || !rc || xbits != cfg->b_dir || rbits != cfg->b_nrm)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "custom books must match the configured bit widths");
+  for (int i = 1; i < (1 << xbits); ++i)
+    if (!(xc[i] >= xc[i - 1])) return fail(OQ_ERR_INVALID_ARGUMENT, "centroids not ascending");
+  for (int i = 1; i < (1 << rbits); ++i)
+    if (!(rc[i] >= rc[i - 1])) return fail(OQ_ERR_INVALID_ARGUMENT, "centroids not ascending");
+  return build_codec(cfg, oqh::custom_book(xc, xbits), oqh::custom_book(rc, rbits), out);
+}
+
+void oq_codec_destroy(oq_codec* c) {
+  if (!c) return;
+  for (void* p : c->allocs) cudaFree(p);
+  delete c;
+}
+
+oq_status oq_codec_config(const oq_codec* c, oq_config* cfg) {
+  if (!c || !cfg) return fail(OQ_ERR_INVALID_ARGUMENT, "null argument");
+  *cfg = c->cfg;
+  return OQ_OK;
+}
+
+oq_status oq_compress(const oq_codec* c, const void* x, int dtype, size_t n, void* records,
+                      void* stream) {
+  oq_status s = check_codec(c);
+  if (s) return s;
+  if (n && (!x || !records)) return fail(OQ_ERR_INVALID_ARGUMENT, "null buffer");
+  if (dtype < OQ_DTYPE_F32 || dtype > OQ_DTYPE_BF16)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "unknown dtype");
+  cudaError_t e = oqd::launch_compress(c->p, x, dtype, n, static_cast<uint8_t*>(records),
+                                       as_stream(stream), c->num_sms);
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "compress kernel");
+}
+
+oq_status oq_decode(const oq_codec* c, const void* records, size_t n, float* out, void* stream) {
+  oq_status s = check_codec(c);
+  if (s) return s;
+  if (n && (!records || !out)) return fail(OQ_ERR_INVALID_ARGUMENT, "null buffer");
+  cudaError_t e = oqd::launch_decode(c->p, static_cast<const uint8_t*>(records), n, out,
+                                     as_stream(stream), c->num_sms);
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "decode kernel");
+}
+
+oq_status oq_wire_header(const oq_config* cfg, uint64_t count, uint8_t h[20]) {
+  oq_status s = validate(cfg);
+  if (s) return s;
+  std::memcpy(h, "OCTO", 4);
+  h[4] = 1;
+  h[5] = cfg->qjl ? 1 : 0;
+  h[6] = cfg->b_dir;
+  h[7] = cfg->b_nrm;
+  std::memcpy(h + 8, &cfg->dim, 4);
+  std::memcpy(h + 12, &count, 8);
+  return OQ_OK;
+}
+
+oq_status oq_wire_parse_header(const uint8_t* p, size_t n, oq_config* cfg, uint64_t* count) {
+  // codec.hpp:410-430 (ByteReader throws FormatError("truncated stream")).
+  if (!p || n < 4) return fail(OQ_ERR_FORMAT, "truncated stream");
+  if (std::memcmp(p, "OCTO", 4) != 0) return fail(OQ_ERR_FORMAT, "bad blob magic");
+  if (n < 5) return fail(OQ_ERR_FORMAT, "truncated stream");
+  if (p[4] != 1) return fail(OQ_ERR_FORMAT, "unsupported blob version");
+  if (n < 6) return fail(OQ_ERR_FORMAT, "truncated stream");
+  if (p[5] & ~1u) return fail(OQ_ERR_FORMAT, "unknown flag bits");
+  if (n < 8) return fail(OQ_ERR_FORMAT, "truncated stream");
+  oq_config c;
+  oq_config_default(&c);
+  c.qjl = p[5] & 1u;
+  c.b_dir = p[6];
+  c.b_nrm = p[7];
+  if (c.b_dir < 1 || c.b_dir > 8 || c.b_nrm < 1 || c.b_nrm > 8)
+    return fail(OQ_ERR_FORMAT, "blob bits out of range");
+  if (n < 12) return fail(OQ_ERR_FORMAT, "truncated stream");
+  std::memcpy(&c.dim, p + 8, 4);
+  if (!is_pow2(c.dim) || c.dim < 4) return fail(OQ_ERR_FORMAT, "blob dim invalid");
+  if (n < 20) return fail(OQ_ERR_FORMAT, "truncated stream");
+  uint64_t cnt;
+  std::memcpy(&cnt, p + 12, 8);
+  const size_t rb = rec_bytes(c);
+  if (n - 20 != cnt * rb) return fail(OQ_ERR_FORMAT, "blob payload size mismatch");
+  if (cfg) *cfg = c;
+  if (count) *count = cnt;
+  return OQ_OK;
+}
+
+oq_status oq_validate_records(const oq_codec* c, const void* records, size_t n, void* stream) {
+  oq_status s = check_codec(c);
+  if (s) return s;
+  if (n == 0) return OQ_OK;
+  int* d_bad = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_bad), sizeof(int), as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  cudaMemsetAsync(d_bad, 0, sizeof(int), as_stream(stream));
+  e = oqd::launch_validate_records(c->p, static_cast<const uint8_t*>(records), n, d_bad,
+                                   as_stream(stream), c->num_sms);
+  int bad = 0;
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, as_stream(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(as_stream(stream));
+  cudaFreeAsync(d_bad, as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "validate kernel");
+  if (bad & 1) return fail(OQ_ERR_FORMAT, "nonzero padding in direction stream");
+  if (bad & 2) return fail(OQ_ERR_FORMAT, "nonzero padding in norm stream");
+  if (bad & 4) return fail(OQ_ERR_FORMAT, "nonzero padding in sign stream");
+  return OQ_OK;
+}
+
+// ---- attention -------------------------------------------------------------
+
+size_t oq_cache_tile_bytes(const oq_codec* c, int role) {
+  return c ? oqd::attention_tile_bytes(c->p, role) : 0;
+}
+
+size_t oq_cache_bytes(const oq_codec* c, int role, uint64_t tokens) {
+  return c ? ((tokens + 31) / 32) * oqd::attention_tile_bytes(c->p, role) : 0;
+}
+
+oq_status oq_cache_pack(const oq_codec* c, int role, const void* records, uint64_t n_streams,
+                        uint64_t n_tokens, uint64_t rec_stride, void* tiles, uint64_t cap_tokens,
+                        void* stream) {
+  oq_status s = check_codec(c);
+  if (s) return s;
+  if (role != OQ_ROLE_K && role != OQ_ROLE_V) return fail(OQ_ERR_INVALID_ARGUMENT, "bad role");
+  if (n_tokens > cap_tokens || n_tokens > rec_stride)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "cache capacity smaller than the token count");
+  if (oqd::attention_tile_bytes(c->p, role) == 0)
+    return fail(OQ_ERR_UNSUPPORTED, "attention tile format needs dim 128 and 2*b_dir+b_nrm <= 13");
+  if (role == OQ_ROLE_V && c->cfg.qjl)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "the V codec carries no QJL sidecar");
+  cudaError_t e = oqd::launch_pack_tiles(c->p, role, static_cast<const uint8_t*>(records),
+                                         n_streams, n_tokens, rec_stride,
+                                         static_cast<uint8_t*>(tiles), (cap_tokens + 31) / 32,
+                                         as_stream(stream));
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "pack tiles kernel");
+}
+
+static size_t parts_per_row(const oq_attn_shape* sh, int n_splits) { (void)sh; return (size_t)n_splits; }
+
+size_t oq_attention_workspace_bytes(const oq_codec* ck, const oq_codec* cv,
+                                    const oq_attn_shape* sh, int n_splits) {
+  if (!ck || !cv || !sh || n_splits < 1) return 0;
+  const size_t rows = (size_t)sh->B * sh->Hq;
+  const size_t part = rows * parts_per_row(sh, n_splits) * (4 + ck->cfg.dim) * sizeof(float);
+  const size_t qf = (size_t)sh->B * sh->Hkv * oqd::attention_qfrag_bytes(ck->p);
+  return ((part + 255) & ~size_t(255)) + qf + 256;
+}
+
+static oq_status attn_check(const oq_codec* ck, const oq_codec* cv, const oq_attn_shape* sh,
+                            const float* q, const void* kc, const void* vc, int n_splits,
+                            size_t ws_bytes) {
+  oq_status s;
+  if ((s = check_codec(ck)) || (s = check_codec(cv))) return s;
+  if (!sh || !q || !kc || !vc) return fail(OQ_ERR_INVALID_ARGUMENT, "null argument");
+  if (sh->B < 1 || sh->Hq < 1 || sh->Hkv < 1 || sh->Hq % sh->Hkv)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "bad head configuration");
+  if (sh->T == 0) return fail(OQ_ERR_INVALID_ARGUMENT, "empty cache");  // attention.hpp:55
+  if (sh->T > sh->cap_tokens) return fail(OQ_ERR_INVALID_ARGUMENT, "values/cache length mismatch");
+  if (n_splits < 1) return fail(OQ_ERR_INVALID_ARGUMENT, "n_splits must be >= 1");
+  if (ck->cfg.dim != cv->cfg.dim) return fail(OQ_ERR_INVALID_ARGUMENT, "K/V dim mismatch");
+  if (cv->cfg.qjl) return fail(OQ_ERR_INVALID_ARGUMENT, "the V codec carries no QJL sidecar");
+  if (!oqd::attention_fast_path_ok(ck->p, cv->p))
+    return fail(OQ_ERR_UNSUPPORTED, "attention kernels need dim 128 and 2*b_dir+b_nrm <= 13");
+  if (ws_bytes < oq_attention_workspace_bytes(ck, cv, sh, n_splits))
+    return fail(OQ_ERR_INVALID_ARGUMENT, "workspace too small");
+  return OQ_OK;
+}
+
+static oq_status run_partials(const oq_codec* ck, const oq_codec* cv, const oq_attn_shape* sh,
+                              const float* q, const void* kc, const void* vc, uint64_t t0,
+                              uint64_t t1, int n_splits, void* ws, cudaStream_t st,
+                              float** parts_out) {
+  const size_t rows = (size_t)sh->B * sh->Hq;
+  const size_t part = rows * (size_t)n_splits * (4 + ck->cfg.dim) * sizeof(float);
+  oqd::AttnArgs a{};
+  a.B = sh->B;
+  a.Hq = sh->Hq;
+  a.Hkv = sh->Hkv;
+  a.T = sh->T;
+  a.t_begin = t0;
+  a.t_end = t1;
+  a.seq_lens = sh->seq_lens;
+  a.q = q;
+  a.kcache = static_cast<const uint8_t*>(kc);
+  a.vcache = static_cast<const uint8_t*>(vc);
+  a.k_tiles_cap = a.v_tiles_cap = (sh->cap_tokens + 31) / 32;
+  a.partials = static_cast<float*>(ws);
+  a.n_parts = n_splits;
+  a.qfrag = static_cast<uint8_t*>(ws) + ((part + 255) & ~size_t(255));
+  cudaError_t e = oqd::launch_attention_partials(ck->p, cv->p, a, n_splits, st, ck->num_sms);
+  if (e != cudaSuccess) return cuda_fail(e, "attention kernel");
+  *parts_out = a.partials;
+  return OQ_OK;
+}
+
+oq_status oq_attention_decode(const oq_codec* ck, const oq_codec* cv, const oq_attn_shape* sh,
+                              const float* q, const void* kc, const void* vc, float* out,
+                              int n_splits, void* ws, size_t ws_bytes, void* stream) {
+  oq_status s = attn_check(ck, cv, sh, q, kc, vc, n_splits, ws_bytes);
+  if (s) return s;
+  if (!out || !ws) return fail(OQ_ERR_INVALID_ARGUMENT, "null argument");
+  float* parts = nullptr;
+  s = run_partials(ck, cv, sh, q, kc, vc, 0, sh->T, n_splits, ws, as_stream(stream), &parts);
+  if (s) return s;
+  const int rows = sh->B * sh->Hq;
+  const size_t w = 4 + ck->cfg.dim;
+  cudaError_t e = oqd::launch_attention_combine(cv->p, parts, rows, n_splits, n_splits * w, w, 1,
+                                                out, as_stream(stream));
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "combine kernel");
+}
+
+oq_status oq_attention_partials(const oq_codec* ck, const oq_codec* cv, const oq_attn_shape* sh,
+                                const float* q, const void* kc, const void* vc, uint64_t t0,
+                                uint64_t t1, float* partial, int n_splits, void* ws,
+                                size_t ws_bytes, void* stream) {
+  oq_status s = attn_check(ck, cv, sh, q, kc, vc, n_splits, ws_bytes);
+  if (s) return s;
+  if (!partial || !ws) return fail(OQ_ERR_INVALID_ARGUMENT, "null argument");
+  if (t0 > t1 || t1 > sh->T) return fail(OQ_ERR_INVALID_ARGUMENT, "bad token range");
+  float* parts = nullptr;
+  s = run_partials(ck, cv, sh, q, kc, vc, t0, t1, n_splits, ws, as_stream(stream), &parts);
+  if (s) return s;
+  const int rows = sh->B * sh->Hq;
+  const size_t w = 4 + ck->cfg.dim;
+  cudaError_t e = oqd::launch_attention_combine(cv->p, parts, rows, n_splits, n_splits * w, w, 0,
+                                                partial, as_stream(stream));
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "combine kernel");
+}
+
+oq_status oq_attention_combine(const oq_codec* cv, const float* partials, int rows, int n_parts,
+                               size_t row_stride, size_t part_stride, int finalize, float* out,
+                               void* stream) {
+  oq_status s = check_codec(cv);
+  if (s) return s;
+  if (!partials || !out || rows < 1 || n_parts < 1)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "bad combine arguments");
+  cudaError_t e = oqd::launch_attention_combine(cv->p, partials, rows, n_parts, row_stride,
+                                                part_stride, finalize, out, as_stream(stream));
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "combine kernel");
+}
+
+}  // extern "C"

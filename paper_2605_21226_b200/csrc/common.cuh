@@ -1,0 +1,92 @@
+// common.cuh — shared device helpers for the sm_100a OCTOPUS kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "codec_params.h"
+
+namespace oqd {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---- exact fp64 primitives (no FMA contraction: every op rounds once, the
+// way the reference's scalar C++ does) -------------------
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+
+// v * (+-1) is exact: flip the sign bit when `neg`.
+__device__ __forceinline__ double dflip(double v, bool neg) {
+  return neg ? __longlong_as_double(__double_as_longlong(v) ^ (long long)0x8000000000000000ull)
+             : v;
+}
+
+// std::upper_bound count over ascending boundaries (lloydmax.hpp:46-49).
+__device__ __forceinline__ uint32_t quantize_ub(const double* b, uint32_t nb, double x) {
+  uint32_t lo = 0, hi = nb;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (!(x < b[mid])) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// io.hpp:115-138 f32 -> f16 RNE, bit-identical (including its NaN payload).
+__device__ __forceinline__ uint16_t f32_to_f16_ref(float f) {
+  const uint32_t x = __float_as_uint(f);
+  const uint32_t sign = (x >> 16) & 0x8000u;
+  const uint32_t ex = (x >> 23) & 0xffu;
+  uint32_t man = x & 0x7fffffu;
+  if (ex == 0xff) return (uint16_t)(sign | 0x7c00u | (man ? 0x200u : 0));
+  const int e = (int)ex - 127 + 15;
+  if (e >= 31) return (uint16_t)(sign | 0x7c00u);
+  if (e <= 0) {
+    if (e < -10) return (uint16_t)sign;
+    man |= 0x800000u;
+    const unsigned sh = (unsigned)(14 - e);
+    uint32_t half = man >> sh;
+    const uint32_t rem = man & ((1u << sh) - 1u);
+    const uint32_t mid = 1u << (sh - 1);
+    if (rem > mid || (rem == mid && (half & 1u))) ++half;
+    return (uint16_t)(sign | half);
+  }
+  uint32_t half = ((uint32_t)e << 10) | (man >> 13);
+  const uint32_t rem = man & 0x1fffu;
+  if (rem > 0x1000u || (rem == 0x1000u && (half & 1u))) ++half;
+  return (uint16_t)(sign | half);
+}
+
+// Load element i of an input row in any supported dtype, widened exactly.
+__device__ __forceinline__ double load_as_double(const void* p, int dtype, size_t i) {
+  switch (dtype) {
+    case OQ_F32: return (double)static_cast<const float*>(p)[i];
+    case OQ_F64: return static_cast<const double*>(p)[i];
+    case OQ_F16: return (double)__half2float(static_cast<const __half*>(p)[i]);
+    default: {  // OQ_BF16
+      const uint16_t b = static_cast<const uint16_t*>(p)[i];
+      return (double)__uint_as_float((uint32_t)b << 16);
+    }
+  }
+}
+
+// Read `bits` (<= 24) starting at bit `pos` of an LSB-first byte stream.
+__device__ __forceinline__ uint32_t read_bits(const uint8_t* s, uint32_t pos, uint32_t bits) {
+  const uint32_t byte = pos >> 3, sh = pos & 7;
+  uint32_t w = (uint32_t)s[byte] | ((uint32_t)s[byte + 1] << 8) | ((uint32_t)s[byte + 2] << 16) |
+               ((uint32_t)s[byte + 3] << 24);
+  return (w >> sh) & ((1u << bits) - 1u);
+}
+
+// Bounds-safe variant for global buffers: bits <= 8 touches at most 2 bytes.
+__device__ __forceinline__ uint32_t read_bits_safe(const uint8_t* s, uint32_t pos, uint32_t bits) {
+  const uint32_t byte = pos >> 3, sh = pos & 7;
+  uint32_t w = s[byte];
+  if (sh + bits > 8) w |= (uint32_t)s[byte + 1] << 8;
+  return (w >> sh) & ((1u << bits) - 1u);
+}
+
+}  // namespace oqd

@@ -1,0 +1,374 @@
+// compress.cu — K1: fused OCTOPUS compress (Encoder::encode, codec.hpp:214-249)
+// on sm_100a, bit-exact against the fp64 CPU reference.
+//
+// Layout: LPV = max(1, D/32) lanes per vector, EPL = D/LPV contiguous
+// elements per lane, all fp64 in registers.  The rotation (signs + WHT) runs
+// in registers (in-lane butterflies for len < EPL, warp shuffles above);
+// rotated coordinates are staged once in shared memory so each lane can pick
+// up whole triplets; octahedral fold, Lloyd-Max bucketing and the joint 3x3
+// search run per lane on its triplets; the QJL epilogue re-runs the rotation
+// on the residual.  Every fp64 op is an explicitly rounded __d*_rn intrinsic
+// in the reference's evaluation order, so the codes are bit-exact (SURVEY.md
+// §7 H1).  Output is the OCTO v1 record (codec.hpp:381-393), assembled
+// byte-parallel in shared memory and stored with coalesced 32-bit writes.
+// The grid is persistent (a few CTAs per SM) so the codebook tables are
+// staged into shared memory once per CTA.
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace oqd {
+
+template <int D>
+struct CompressShape {
+  static constexpr int LPV = D <= 32 ? 1 : D / 32;
+  static constexpr int EPL = D / LPV;
+  static constexpr int NT = (D + 2) / 3;
+  static constexpr int TPL = (NT + LPV - 1) / LPV;  // triplets per lane
+  static constexpr int THREADS = 128;
+  static constexpr int VPC = THREADS / LPV;          // vectors per CTA
+  // padded element index: a 4-double gap after each lane chunk keeps the
+  // 16 lanes of a half-warp on distinct 8-byte banks.
+  __host__ __device__ static constexpr int pidx(int e) { return LPV > 1 ? e + 4 * (e / EPL) : e; }
+  static constexpr int NEED = pidx(3 * NT - 1) + 1;
+  static constexpr int STRIDE = LPV > 1 ? ((NEED + 14) / 16) * 16 + 1 : (NEED | 1);
+};
+
+struct CompressSmem {
+  double* xb;
+  double* rb;
+  double* rc;
+  const double* dirs;
+};
+
+// ---- joint rounding of one triplet (codec.hpp:143-195) -------------------
+__device__ __forceinline__ void oct_encode_exact(double t0, double t1, double t2, double& xi,
+                                                 double& eta) {
+  // octahedral.hpp:22-31
+  const double l1 = dadd(dadd(fabs(t0), fabs(t1)), fabs(t2));
+  const double inv = ddiv(1.0, l1 > 1e-12 ? l1 : 1e-12);
+  const double px = dmul(t0, inv), py = dmul(t1, inv), pz = dmul(t2, inv);
+  if (pz >= 0.0) {
+    xi = px;
+    eta = py;
+  } else {
+    xi = dflip(dsub(1.0, fabs(py)), !(px >= 0.0));
+    eta = dflip(dsub(1.0, fabs(px)), !(py >= 0.0));
+  }
+}
+
+__device__ __forceinline__ double dot3_exact(double t0, double t1, double t2, const double* n) {
+  return dadd(dadd(dmul(t0, n[0]), dmul(t1, n[1])), dmul(t2, n[2]));
+}
+
+__device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const CompressSmem& s,
+                                                double t0, double t1, double t2) {
+  double xi, eta;
+  oct_encode_exact(t0, t1, t2, xi, eta);
+  const uint32_t K = p.K;
+  const uint32_t sx = quantize_ub(s.xb, K - 1, xi);
+  const uint32_t sy = quantize_ub(s.xb, K - 1, eta);
+  if (p.rounding == 0) {
+    double r = dsqrt(dadd(dadd(dmul(t0, t0), dmul(t1, t1)), dmul(t2, t2)));
+    r = r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r);
+    const uint32_t ir = quantize_ub(s.rb, p.KR - 1, r);
+    return sx | (sy << 8) | (ir << 16);
+  }
+  uint32_t ax0 = sx, ax1 = sx, ay0 = sy, ay1 = sy;
+  if (p.rounding == 1) {
+    ax1 = min(sx + 1, K - 1);
+    ay1 = min(sy + 1, K - 1);
+  } else if (p.rounding == 2) {
+    ax0 = sx > 0 ? sx - 1 : 0;
+    ay0 = sy > 0 ? sy - 1 : 0;
+    ax1 = min(sx + 1, K - 1);
+    ay1 = min(sy + 1, K - 1);
+  } else {
+    ax0 = ay0 = 0;
+    ax1 = ay1 = K - 1;
+  }
+  double best = -__longlong_as_double(0x7ff0000000000000ll);  // -inf
+  uint32_t bx = ax0, by = ay0;
+  for (uint32_t a = ax0; a <= ax1; ++a)
+    for (uint32_t b = ay0; b <= ay1; ++b) {
+      const double sc = dot3_exact(t0, t1, t2, s.dirs + 3 * (a * K + b));
+      if (sc > best) {  // strict: ties keep the first row-major pair
+        best = sc;
+        bx = a;
+        by = b;
+      }
+    }
+  const double cl = best < 0.0 ? 0.0 : (best > 1.0 ? 1.0 : best);
+  const uint32_t ir = quantize_ub(s.rb, p.KR - 1, cl);
+  return bx | (by << 8) | (ir << 16);
+}
+
+// ---- in-register rotation: y = H (s .* x) * inv_sqrt_d (rotation.hpp:46-49)
+template <int D>
+__device__ __forceinline__ void rotate_exact(double (&x)[CompressShape<D>::EPL], uint32_t smask,
+                                             int sub, double scale) {
+  using S = CompressShape<D>;
+#pragma unroll
+  for (int i = 0; i < S::EPL; ++i) x[i] = dflip(x[i], (smask >> i) & 1u);
+#pragma unroll
+  for (int len = 1; len < S::EPL; len <<= 1) {
+#pragma unroll
+    for (int i = 0; i < S::EPL; ++i)
+      if (!(i & len)) {
+        const double a = x[i], b = x[i + len];
+        x[i] = dadd(a, b);
+        x[i + len] = dsub(a, b);
+      }
+  }
+#pragma unroll
+  for (int lm = 1; lm < S::LPV; lm <<= 1) {
+    const bool upper = sub & lm;
+#pragma unroll
+    for (int i = 0; i < S::EPL; ++i) {
+      const double o = __shfl_xor_sync(kFull, x[i], lm);
+      // element j (lower lane) pairs with j+len (upper lane): (a+b, a-b)
+      x[i] = upper ? dsub(o, x[i]) : dadd(x[i], o);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < S::EPL; ++i) x[i] = dmul(x[i], scale);
+}
+
+// Sequential sum of squares over the whole vector, in element order
+// (codec.hpp:219-220 / qjl.hpp:28-29): the chain walks lane 0..LPV-1.
+template <int D>
+__device__ __forceinline__ double seq_sumsq(const double (&x)[CompressShape<D>::EPL], int sub,
+                                            int lane) {
+  using S = CompressShape<D>;
+  double run = 0.0;
+#pragma unroll
+  for (int L = 0; L < S::LPV; ++L) {
+    if (sub == L) {
+#pragma unroll
+      for (int i = 0; i < S::EPL; ++i) run = dadd(run, dmul(x[i], x[i]));
+    }
+    if (S::LPV > 1) run = __shfl_sync(kFull, run, (lane & ~(S::LPV - 1)) + L);
+  }
+  return run;
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const void* __restrict__ x,
+                                                       int dtype, size_t n,
+                                                       uint8_t* __restrict__ out, int aligned) {
+  using S = CompressShape<D>;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int sub = S::LPV > 1 ? (lane & (S::LPV - 1)) : 0;
+  const int vl = tid / S::LPV;  // vector slot within the CTA
+
+  // ---- carve shared memory ------------------------------------------------
+  uint8_t* sp = smem_raw;
+  double* ur_s = reinterpret_cast<double*>(sp);
+  sp += sizeof(double) * S::VPC * S::STRIDE;
+  double* xb_s = reinterpret_cast<double*>(sp);
+  sp += sizeof(double) * 256;
+  double* rb_s = reinterpret_cast<double*>(sp);
+  sp += sizeof(double) * 256;
+  double* rc_s = reinterpret_cast<double*>(sp);
+  sp += sizeof(double) * 256;
+  const uint32_t kk = p.K * p.K;
+  const bool dirs_in_smem = kk <= 1024;
+  double* dirs_s = reinterpret_cast<double*>(sp);
+  if (dirs_in_smem) sp += sizeof(double) * 3 * kk;
+  float* gam_s = reinterpret_cast<float*>(sp);
+  sp += sizeof(float) * S::VPC;
+  uint32_t* sgn_s = reinterpret_cast<uint32_t*>(sp);  // QJL: D/32 words (>=1) per vector
+  constexpr int SGW = D >= 32 ? D / 32 : 1;
+  sp += sizeof(uint32_t) * S::VPC * SGW;
+  uint16_t* gr_s = reinterpret_cast<uint16_t*>(sp);
+  sp += sizeof(uint16_t) * S::VPC;
+  uint16_t* dcode_s = reinterpret_cast<uint16_t*>(sp);  // [VPC][2*NT]
+  sp += sizeof(uint16_t) * S::VPC * 2 * S::NT;
+  uint8_t* ncode_s = sp;  // [VPC][NT]
+  sp += S::VPC * S::NT;
+  sp = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sp) + 15) & ~uintptr_t(15));
+  uint8_t* stage_s = sp;  // [VPC * rec_bytes]
+
+  for (uint32_t i = tid; i < p.K - 1; i += blockDim.x) xb_s[i] = p.xi_bnd[i];
+  for (uint32_t i = tid; i < p.KR - 1; i += blockDim.x) rb_s[i] = p.rho_bnd[i];
+  for (uint32_t i = tid; i < p.KR; i += blockDim.x) rc_s[i] = p.rho_c[i];
+  if (dirs_in_smem)
+    for (uint32_t i = tid; i < 3 * kk; i += blockDim.x) dirs_s[i] = p.dirs64[i];
+  __syncthreads();
+  CompressSmem sm{xb_s, rb_s, rc_s, dirs_in_smem ? dirs_s : p.dirs64};
+
+  const uint32_t smask = p.sign_mask[(sub * S::EPL) >> 5] >> ((sub * S::EPL) & 31);
+  const uint32_t qmask = p.qsign_mask[(sub * S::EPL) >> 5] >> ((sub * S::EPL) & 31);
+  const size_t nblocks = (n + S::VPC - 1) / S::VPC;
+  const uint32_t rb = p.rec_bytes;
+
+  for (size_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+    const size_t v = blk * S::VPC + vl;
+    const bool live = v < n;
+    double* ur = ur_s + vl * S::STRIDE;
+
+    // ---- load, norm, normalize (codec.hpp:219-225) ------------------------
+    double xv[S::EPL];
+#pragma unroll
+    for (int i = 0; i < S::EPL; ++i)
+      xv[i] = live ? load_as_double(x, dtype, v * D + sub * S::EPL + i) : 0.0;
+    const double g2 = seq_sumsq<D>(xv, sub, lane);
+    const double gamma = dsqrt(g2);
+    const double inv = ddiv(1.0, gamma > 1e-12 ? gamma : 1e-12);
+#pragma unroll
+    for (int i = 0; i < S::EPL; ++i) xv[i] = dmul(xv[i], inv);
+    // ---- rotate (codec.hpp:227) -------------------------------------------
+    rotate_exact<D>(xv, smask, sub, p.inv_sqrt_d);
+#pragma unroll
+    for (int i = 0; i < S::EPL; ++i) ur[S::pidx(sub * S::EPL + i)] = xv[i];
+    if (sub == S::LPV - 1)  // zero pad to 3 * n_tri (codec.hpp:229-230)
+      for (int e = D; e < 3 * S::NT; ++e) ur[S::pidx(e)] = 0.0;
+    if (sub == 0) gam_s[vl] = (float)gamma;  // codec.hpp:233 (double -> float RN)
+    __syncwarp();
+
+    // ---- per-triplet joint rounding (codec.hpp:236-241) -------------------
+    double tv[3 * S::TPL];
+    uint32_t code[S::TPL];
+#pragma unroll
+    for (int u = 0; u < S::TPL; ++u) {
+      const int t = sub * S::TPL + u;
+      if (t < S::NT) {
+        tv[3 * u] = ur[S::pidx(3 * t)];
+        tv[3 * u + 1] = ur[S::pidx(3 * t + 1)];
+        tv[3 * u + 2] = ur[S::pidx(3 * t + 2)];
+        code[u] = joint_round(p, sm, tv[3 * u], tv[3 * u + 1], tv[3 * u + 2]);
+        dcode_s[vl * 2 * S::NT + 2 * t] = (uint16_t)(code[u] & 0xff);
+        dcode_s[vl * 2 * S::NT + 2 * t + 1] = (uint16_t)((code[u] >> 8) & 0xff);
+        ncode_s[vl * S::NT + t] = (uint8_t)(code[u] >> 16);
+      }
+    }
+
+    if (p.qjl) {
+      // ---- QJL epilogue (codec.hpp:243-247, qjl.hpp:23-36) ------------------
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < S::TPL; ++u) {
+        const int t = sub * S::TPL + u;
+        if (t < S::NT) {
+          const uint32_t a = code[u] & 0xff, b = (code[u] >> 8) & 0xff, ir = code[u] >> 16;
+          const double* nv = sm.dirs + 3 * (a * p.K + b);
+          const double r = sm.rc[ir];
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            if (3 * t + j < D) ur[S::pidx(3 * t + j)] = dsub(tv[3 * u + j], dmul(r, nv[j]));
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < S::EPL; ++i) xv[i] = ur[S::pidx(sub * S::EPL + i)];
+      const double n2 = seq_sumsq<D>(xv, sub, lane);
+      rotate_exact<D>(xv, qmask, sub, p.inv_sqrt_d);
+      uint32_t bits = 0;
+#pragma unroll
+      for (int i = 0; i < S::EPL; ++i) bits |= (xv[i] >= 0.0 ? 1u : 0u) << i;
+      if (S::EPL >= 32) sgn_s[vl * SGW + sub] = bits;
+      else sgn_s[vl * SGW] = bits;
+      if (sub == 0) gr_s[vl] = f32_to_f16_ref((float)dsqrt(n2));
+    }
+    __syncthreads();
+
+    // ---- byte-parallel OCTO record assembly (codec.hpp:381-393) -----------
+    const size_t nv = min((size_t)S::VPC, n - blk * S::VPC);
+    const int warp = tid >> 5, nwarps = blockDim.x >> 5;
+    for (int w = warp; w < (int)nv; w += nwarps) {
+      const uint16_t* dc = dcode_s + w * 2 * S::NT;
+      const uint8_t* nc = ncode_s + w * S::NT;
+      for (uint32_t off = lane; off < rb; off += 32) {
+        uint32_t byte = 0;
+        if (off < 4) {
+          byte = (__float_as_uint(gam_s[w]) >> (8 * off)) & 0xff;
+        } else if (off < 4 + p.dir_bytes) {
+          const int j = off - 4, bd = p.b_dir;
+          const int f0 = (8 * j) / bd, f1 = min((8 * j + 7) / bd, 2 * S::NT - 1);
+          for (int f = f0; f <= f1; ++f) {
+            const int sh = f * bd - 8 * j;
+            const uint32_t c = dc[f];
+            byte |= sh >= 0 ? (c << sh) : (c >> -sh);
+          }
+        } else if (off < 4 + p.dir_bytes + p.nrm_bytes) {
+          const int j = off - 4 - p.dir_bytes, bn = p.b_nrm;
+          const int f0 = (8 * j) / bn, f1 = min((8 * j + 7) / bn, S::NT - 1);
+          for (int f = f0; f <= f1; ++f) {
+            const int sh = f * bn - 8 * j;
+            const uint32_t c = nc[f];
+            byte |= sh >= 0 ? (c << sh) : (c >> -sh);
+          }
+        } else {
+          const int j = off - 4 - p.dir_bytes - p.nrm_bytes;
+          if (j < 2) byte = (gr_s[w] >> (8 * j)) & 0xff;
+          else byte = (sgn_s[w * SGW + ((j - 2) >> 2)] >> (8 * ((j - 2) & 3))) & 0xff;
+        }
+        stage_s[w * rb + off] = (uint8_t)(byte & 0xff);
+      }
+    }
+    __syncthreads();
+    const size_t nbytes = nv * rb;
+    uint8_t* dst = out + blk * S::VPC * (size_t)rb;
+    if (aligned) {
+      const uint32_t* src32 = reinterpret_cast<const uint32_t*>(stage_s);
+      uint32_t* dst32 = reinterpret_cast<uint32_t*>(dst);
+      for (size_t i = tid; i < nbytes / 4; i += blockDim.x) dst32[i] = src32[i];
+      for (size_t i = (nbytes / 4) * 4 + tid; i < nbytes; i += blockDim.x) dst[i] = stage_s[i];
+    } else {
+      for (size_t i = tid; i < nbytes; i += blockDim.x) dst[i] = stage_s[i];
+    }
+    __syncthreads();
+  }
+}
+
+template <int D>
+static size_t compress_smem(const OqCodecParams& p) {
+  using S = CompressShape<D>;
+  const uint32_t kk = p.K * p.K;
+  size_t b = sizeof(double) * S::VPC * S::STRIDE + 3 * sizeof(double) * 256;
+  if (kk <= 1024) b += sizeof(double) * 3 * kk;
+  b += sizeof(float) * S::VPC + sizeof(uint32_t) * S::VPC * (D >= 32 ? D / 32 : 1) +
+       sizeof(uint16_t) * S::VPC + sizeof(uint16_t) * S::VPC * 2 * S::NT + S::VPC * S::NT;
+  b = (b + 15) & ~size_t(15);
+  b += (size_t)S::VPC * p.rec_bytes + 16;
+  return b;
+}
+
+template <int D>
+static cudaError_t launch_compress_d(const OqCodecParams& p, const void* x, int dtype, size_t n,
+                                     uint8_t* out, cudaStream_t st, int num_sms) {
+  using S = CompressShape<D>;
+  const size_t smem = compress_smem<D>(p);
+  cudaError_t e = cudaFuncSetAttribute(compress_kernel<D>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compress_kernel<D>, S::THREADS, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const size_t nblocks = (n + S::VPC - 1) / S::VPC;
+  size_t grid = (size_t)per_sm * num_sms;
+  if (grid > nblocks) grid = nblocks;
+  const int aligned = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
+  compress_kernel<D><<<(unsigned)grid, S::THREADS, smem, st>>>(p, x, dtype, n, out, aligned);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, size_t n,
+                            uint8_t* out, cudaStream_t st, int num_sms) {
+  if (n == 0) return cudaSuccess;
+  switch (p.dim) {
+    case 4: return launch_compress_d<4>(p, x, dtype, n, out, st, num_sms);
+    case 8: return launch_compress_d<8>(p, x, dtype, n, out, st, num_sms);
+    case 16: return launch_compress_d<16>(p, x, dtype, n, out, st, num_sms);
+    case 32: return launch_compress_d<32>(p, x, dtype, n, out, st, num_sms);
+    case 64: return launch_compress_d<64>(p, x, dtype, n, out, st, num_sms);
+    case 128: return launch_compress_d<128>(p, x, dtype, n, out, st, num_sms);
+    case 256: return launch_compress_d<256>(p, x, dtype, n, out, st, num_sms);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace oqd

@@ -1,0 +1,56 @@
+// kernels.h — launcher declarations for the sm_100a kernels (host side).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "codec_params.h"
+
+namespace oqd {
+
+// K1: Encoder::encode -> OCTO v1 records.
+cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, size_t n,
+                            uint8_t* out, cudaStream_t st, int num_sms);
+// K2: Encoder::decode of OCTO v1 records -> fp32 [n, dim].
+cudaError_t launch_decode(const OqCodecParams& p, const uint8_t* recs, size_t n, float* out,
+                          cudaStream_t st, int num_sms);
+// Wire validation: zero padding bits in every record (codec.hpp:447,455,459-461).
+// Sets *bad (device int) nonzero on any violation.
+cudaError_t launch_validate_records(const OqCodecParams& p, const uint8_t* recs, size_t n,
+                                    int* bad, cudaStream_t st, int num_sms);
+
+// ---- compressed-cache attention (attention.cu) ----------------------------
+struct AttnArgs {
+  int B, Hq, Hkv;        // batch, query heads, kv heads (Hq % Hkv == 0)
+  size_t T;              // tokens in the cache (per sequence)
+  size_t t_begin, t_end; // token range processed by this call (sharding)
+  const int32_t* seq_lens;  // optional per-sequence lengths (device), else T
+  const float* q;        // [B, Hq, D] fp32 (device)
+  const uint8_t* kcache; // K tiles [B][Hkv][T/32][ktile_bytes]
+  const uint8_t* vcache; // V tiles [B][Hkv][T/32][vtile_bytes]
+  size_t k_tiles_cap, v_tiles_cap;  // tiles allocated per (b, kv head)
+  float* partials;       // [B*Hq][n_parts][2 + D] (m, l, acc) scratch
+  int n_parts;           // split-K partial slots per (b, q head)
+  float* out;            // [B, Hq, D] fp32 (combine output)
+  void* qfrag;           // [B*Hkv] fragment scratch (attention_qfrag_bytes each)
+};
+
+size_t attention_tile_bytes(const OqCodecParams& p, int role);  // role 0 = K, 1 = V
+size_t attention_qfrag_bytes(const OqCodecParams& pk);
+bool attention_fast_path_ok(const OqCodecParams& pk, const OqCodecParams& pv);
+// records (one (b, kv-head) stream of n tokens) -> tiles
+cudaError_t launch_pack_tiles(const OqCodecParams& p, int role, const uint8_t* recs,
+                              size_t n_streams, size_t n_tokens, size_t rec_stride_tokens,
+                              uint8_t* tiles, size_t tiles_cap, cudaStream_t st);
+// split-K partials over [t_begin, t_end) (K5 prologue + K3)
+cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecParams& pv,
+                                      const AttnArgs& a, int splits, cudaStream_t st,
+                                      int num_sms);
+// K4: merge n_parts partials in order, inverse V rotation, divide by l.
+// partials[row*row_stride + part*part_stride + (m, l, acc[D])]; finalize=0
+// writes the merged (m, l, acc) partial instead of the output.
+cudaError_t launch_attention_combine(const OqCodecParams& pv, const float* partials, int rows,
+                                     int n_parts, size_t row_stride, size_t part_stride,
+                                     int finalize, float* out, cudaStream_t st);
+
+}  // namespace oqd
