@@ -1,0 +1,441 @@
+#!/usr/bin/env python
+"""bench.py — OCTOPUS compressed-KV decode attention (and compress) on B200.
+
+Contract:
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c3|c4|c5]
+prints ONE JSON line on rank 0.
+
+Headline workload (BASELINE.json configs[2], "C3"): Qwen2.5-7B-shaped decode
+attention, B=8, 28 query / 4 KV heads, d=128, K=V 3-bit (b_dir 4, b_nrm 2),
+131072 cached tokens per rank.  A "step" = one decode-attention pass over the
+whole compressed cache (qprep + fused split-K attention + combine; with N>1
+ranks the cache is sequence-sharded: rank r holds its own 128K-token slice of
+an N*128K context and the partial (m, l, acc) states meet in ONE NCCL
+all-gather, then every rank merges them -> weak scaling).
+value = algorithmic compressed-KV bytes of all ranks (B*Hkv*T*(58+58) B per
+rank) / max-over-ranks step time.  Inputs (486 MB per rank) exceed the 126 MB
+L2, so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE_METRIC = ("decode-attn compressed-KV GB/s (% HBM peak) & compress tokens/s, "
+                   "1/2/4/8 B200")
+
+WORKLOADS = {
+    # name: (bits, qjl_on_K, B, Hq, Hkv, T_per_rank, description)
+    "c3": (3, False, 8, 28, 4, 131072, "C3: Qwen2.5-7B-shape decode attention, 3-bit K=V, "
+                                       "128K tokens/rank, B=8"),
+    "c4": (2, True, 32, 28, 4, 32768, "C4: OCTOPUS-QJL 2-bit K (+1-bit residual signs), "
+                                      "2-bit V, 32K tokens/rank, B=32"),
+    "c5": (2, False, 8, 28, 4, 131072, "C5: 2-bit K=V, 128K tokens/rank (1M-token context at "
+                                       "8 ranks), B=8"),
+}
+
+
+def rec_bytes(bits, qjl):
+    bd, bn = bits + 1, bits - 1
+    r = 4 + (86 * bd + 7) // 8 + (43 * bn + 7) // 8
+    return r + (18 if qjl else 0)
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """Poll NVML SM clocks + throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self.samples, self.reasons = [], 0
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        r = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max, "samples": len(self.samples), "reasons": r}
+
+
+# ---------------------------------------------------------------------------
+def build_cache(oq, torch, dev, bits, qjl, B, Hkv, T, seed, keep_host=0):
+    """Synthetic Gaussian K/V, compressed by K1 on the device, packed in tiles.
+
+    Returns the cache plus (optionally) the first `keep_host` streams' records
+    on the host for the CPU baseline.
+    """
+    bd, bn = oq.default_bit_split(bits)
+    ek = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=1000 + seed, qjl=qjl,
+                                   qjl_seed=2000 + seed))
+    ev = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=3000 + seed))
+    cache = oq.KVCache(ek, ev, B, Hkv, T)
+    g = torch.Generator(device=dev).manual_seed(seed)
+    streams = B * Hkv
+    per = max(1, (1 << 21) // T)  # streams per chunk (~2M vectors)
+    host = {"k": [], "v": []}
+    for s0 in range(0, streams, per):
+        ns = min(per, streams - s0)
+        k = torch.randn((ns * T, 128), device=dev, generator=g)
+        v = torch.randn((ns * T, 128), device=dev, generator=g)
+        kr = ek.compress(k)
+        vr = ev.compress(v)
+        del k, v
+        # pack this chunk of streams into the cache tiles
+        ktb, vtb = ek.tile_bytes(0), ev.tile_bytes(1)
+        ntile = (T + 31) // 32
+        kt = cache.k[s0 * ntile * ktb:(s0 + ns) * ntile * ktb]
+        vt = cache.v[s0 * ntile * vtb:(s0 + ns) * ntile * vtb]
+        L = oq.lib()
+        oq._check(L.oq_cache_pack(ek.handle, 0, oq._ptr(kr), ns, T, T, oq._ptr(kt), T,
+                                  oq._stream()))
+        oq._check(L.oq_cache_pack(ev.handle, 1, oq._ptr(vr), ns, T, T, oq._ptr(vt), T,
+                                  oq._stream()))
+        for i in range(ns):
+            if s0 + i < keep_host:
+                host["k"].append(kr[i * T:(i + 1) * T].cpu().numpy())
+                host["v"].append(vr[i * T:(i + 1) * T].cpu().numpy())
+        del kr, vr
+    cache.tokens = T
+    torch.cuda.synchronize()
+    return cache, host
+
+
+def cpu_reference_sample(ref_lib, bits, qjl, seed, k_recs, v_recs, q, threads):
+    """One bounded sample of the workload on the reference CPU implementation:
+    Encoder::decode of the V records + attention_decode for every query head
+    of the sampled KV streams (fan-out over heads).  Returns (seconds, bytes)."""
+    bd, bn = bits + 1, bits - 1
+    ek = ref_lib.encoder(b_dir=bd, b_nrm=bn, rotation_seed=1000 + seed, qjl=qjl,
+                         qjl_seed=2000 + seed)
+    ev = ref_lib.encoder(b_dir=bd, b_nrm=bn, rotation_seed=3000 + seed)
+    n_streams = len(k_recs)
+    G = q.shape[1] // n_streams if q.ndim == 3 else q.shape[0] // n_streams
+    qh = q.reshape(n_streams, G, 128).astype(np.float64)
+    t0 = time.perf_counter()
+    res = [None] * n_streams
+
+    def work(s):
+        vals = ev.decode(v_recs[s], threads=max(1, threads // n_streams))
+        res[s] = ek.attention(qh[s], k_recs[s], vals, 1, threads=G)
+
+    ths = [threading.Thread(target=work, args=(s,)) for s in range(n_streams)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    dt = time.perf_counter() - t0
+    nbytes = sum(len(k) * (k.shape[1] + v_recs[i].shape[1]) for i, k in enumerate(k_recs))
+    return dt, nbytes
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    compiled from /root/reference/proj/include) on this host's cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import RefLib
+    bits, qjl, B, Hq, Hkv, T, desc = WORKLOADS[args.config]
+    ref = RefLib()
+    cores = os.cpu_count() or 1
+    Ts = min(T, 32768)
+    rng = np.random.default_rng(7)
+    bd, bn = bits + 1, bits - 1
+    seed = 0
+    ek = ref.encoder(b_dir=bd, b_nrm=bn, rotation_seed=1000 + seed, qjl=qjl, qjl_seed=2000 + seed)
+    ev = ref.encoder(b_dir=bd, b_nrm=bn, rotation_seed=3000 + seed)
+    k_recs = [ek.encode_f32(rng.standard_normal((Ts, 128), np.float32), threads=cores)
+              for _ in range(Hkv)]
+    v_recs = [ev.encode_f32(rng.standard_normal((Ts, 128), np.float32), threads=cores)
+              for _ in range(Hkv)]
+    q = rng.standard_normal((Hq, 128)).astype(np.float32)
+    for _ in range(max(1, args.warmup)):
+        cpu_reference_sample(ref, bits, qjl, seed, k_recs, v_recs, q, cores)
+    ts, nb = [], 0
+    for _ in range(args.steps):
+        dt, nb = cpu_reference_sample(ref, bits, qjl, seed, k_recs, v_recs, q, cores)
+        ts.append(dt)
+    tot = sum(ts)
+    gbs = nb * len(ts) / tot / 1e9
+    sample = (f"1 batch entry x {Hkv} KV streams x {Ts} tokens x {Hq} query heads "
+              f"(Encoder::decode of V + attention_decode per head)")
+    line = {
+        "impl": "reference", "metric": BASELINE_METRIC, "value": gbs, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(ts), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic Gaussian (numpy)",
+        "config": workload_config(args, 1, None),
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, world, splits):
+    bits, qjl, B, Hq, Hkv, T, desc = WORKLOADS[args.config]
+    return {"workload": desc, "B": B, "Hq": Hq, "Hkv": Hkv, "d": 128, "bits": bits,
+            "b_dir": bits + 1, "b_nrm": bits - 1, "rounding": "local3x3", "qjl_on_K": qjl,
+            "tokens_per_rank": T, "context_tokens": T * world,
+            "record_bytes_K": rec_bytes(bits, qjl), "record_bytes_V": rec_bytes(bits, False),
+            "splits": splits, "parallelism": f"sequence-sharded x{world} (NCCL all-gather of "
+                                             "softmax partials)" if world > 1 else "single GPU",
+            "l2": "no flush: per-rank inputs > 126 MB L2"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compress", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_21226_b200 as oq
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    bits, qjl, B, Hq, Hkv, T, desc = WORKLOADS[args.config]
+    keep = Hkv if (rank == 0 and world == 1 and not args.no_cpu_baseline) else 0
+    cache, host = build_cache(oq, torch, dev, bits, qjl, B, Hkv, T, seed=rank, keep_host=keep)
+    rows = B * Hq
+    q_host = torch.randn((B, Hq, 128), generator=torch.Generator().manual_seed(99)).pin_memory()
+    q = q_host.to(dev)
+    splits = oq.default_splits(B, Hkv, Hq, T)
+    stream = torch.cuda.current_stream()
+    gathered = torch.empty((world, rows, 132), dtype=torch.float32, device=dev)
+    out = torch.empty((B, Hq, 128), dtype=torch.float32, device=dev)
+
+    def step(qd):
+        if world == 1:
+            return oq.attention_decode(qd, cache, n_splits=splits, out=out)
+        part = oq.attention_partials(qd, cache, 0, T, n_splits=splits)
+        dist.all_gather_into_tensor(gathered, part)
+        return oq.attention_combine(cache.enc_v, gathered, rows, world, 132, rows * 132,
+                                    out=out.view(rows, 128))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step(q)
+    torch.cuda.synchronize()
+
+    # ---- device-timed region ----------------------------------------------------
+    oq.timing(True)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(q)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    k_ms, k_n = oq.timing_collect("attention")
+    oq.timing(False)
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+
+    alg_bytes_rank = B * Hkv * T * (rec_bytes(bits, qjl) + rec_bytes(bits, False))
+    value = world * alg_bytes_rank * args.steps / (ms * 1e-3) / 1e9
+    peak, peak_kind = measured_peaks()
+    kern_ms = k_ms / max(1, k_n)
+    achieved = alg_bytes_rank / (kern_ms * 1e-3) / 1e9
+
+    # ---- end to end through the public API with host buffers --------------------
+    out_host = torch.empty((B, Hq, 128), dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        qd = q_host.to(dev, non_blocking=True)
+        out_host.copy_(step(qd).view(B, Hq, 128), non_blocking=True)
+    torch.cuda.synchronize()
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        qd = q_host.to(dev, non_blocking=True)
+        out_host.copy_(step(qd).view(B, Hq, 128), non_blocking=True)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t = torch.tensor([e2.elapsed_time(e3)], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    e2e_val = world * alg_bytes_rank * args.steps / (e2e_ms * 1e-3) / 1e9
+
+    # ---- compress (BASELINE configs[1]: 2^20 keys, fp32 in) ----------------------
+    comp = None
+    if not args.no_compress:
+        comp = bench_compress(oq, torch, dev, bits, world, barrier, dist, peak)
+
+    # ---- CPU baseline: the reference implementation on this host ----------------
+    cpu = None
+    if keep:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_bind import RefLib
+        ref = RefLib()
+        cores = os.cpu_count() or 1
+        Ts = min(T, 32768)
+        kr = [h[:Ts] for h in host["k"]]
+        vr = [h[:Ts] for h in host["v"]]
+        qs = q_host[0].numpy()
+        dts, nb = [], 0
+        t_end = time.perf_counter() + 8.0
+        while time.perf_counter() < t_end or not dts:
+            dt, nb = cpu_reference_sample(ref, bits, qjl, rank, kr, vr, qs, cores)
+            dts.append(dt)
+        cpu = {"value": nb * len(dts) / sum(dts) / 1e9, "unit": "GB/s", "cores": cores,
+               "kind": "reference",
+               "sample": f"batch entry 0: {Hkv} KV streams x {Ts} tokens x {Hq} query heads, "
+                         f"V decoded by Encoder::decode + attention_decode per head; "
+                         f"{len(dts)} repeats, {sum(dts):.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": BASELINE_METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8 codes -> f16 mma, f32 accumulate",
+            "data": "synthetic (torch.randn K/V/Q, K/V compressed on device by K1)",
+            "config": workload_config(args, world, splits),
+            "hbm_frac_of_peak": value / world / peak,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+                         "kernel": "attn_partials_kernel (K3)",
+                         "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": alg_bytes_rank},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": q_host.numel() * 4,
+                    "d2h_bytes_per_step": out_host.numel() * 4,
+                    "what": "pinned q H2D + public-API attention + out D2H per step; KV cache "
+                            "device-resident"},
+            "clocks": clk.summary(),
+            "gpu_launches": (3 if world == 1 else 3) * args.steps,
+            "compress": comp,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def bench_compress(oq, torch, dev, bits, world, barrier, dist, peak):
+    """K1 at BASELINE configs[1]: 2^20 fp32 keys -> OCTO records, bit-exact."""
+    n = 1 << 20
+    bd, bn = oq.default_bit_split(bits)
+    enc = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn))
+    x = torch.randn((n, 128), device=dev, generator=torch.Generator(device=dev).manual_seed(5))
+    recs = torch.empty((n, enc.record_bytes), dtype=torch.uint8, device=dev)
+    dec = torch.empty((n, 128), dtype=torch.float32, device=dev)
+    for _ in range(3):
+        enc.compress(x, out=recs)
+        enc.decode(recs, out=dec)
+    torch.cuda.synchronize()
+    steps = 10
+    oq.timing(True)
+    for _ in range(steps):
+        enc.compress(x, out=recs)
+        enc.decode(recs, out=dec)
+    c_ms, c_n = oq.timing_collect("compress")
+    d_ms, d_n = oq.timing_collect("decode")
+    oq.timing(False)
+    t = torch.tensor([c_ms / c_n, d_ms / d_n], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    cm, dm = (float(v) for v in t.tolist())
+    nbytes = n * (512 + enc.record_bytes)
+    return {"metric": "compress tokens/s", "value": world * n / (cm * 1e-3), "unit": "tokens/s",
+            "config": {"workload": "C2: 2^20 keys d=128 fp32 in, local3x3, OCTO records out",
+                       "bits": bits},
+            "ms": cm, "gbs": nbytes / (cm * 1e-3) / 1e9, "frac_of_hbm": nbytes / (cm * 1e-3) / 1e9
+            / peak,
+            "decode": {"metric": "decode tokens/s", "value": world * n / (dm * 1e-3), "ms": dm,
+                       "gbs": nbytes / (dm * 1e-3) / 1e9,
+                       "frac_of_hbm": nbytes / (dm * 1e-3) / 1e9 / peak}}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -150,6 +150,12 @@ oq_status oq_attention_combine(const oq_codec* cv, const float* partials, int ro
                                size_t row_stride, size_t part_stride, int finalize, float* out,
                                void* stream);
 
+/* ---- measurement support (bench.py) -------------------------------------
+ * When enabled, CUDA events are recorded on the launching stream around each
+ * hot kernel ("compress", "decode", "attention"); collect sums them. */
+void oq_timing_enable(int on);
+oq_status oq_timing_collect(const char* name, double* total_ms, int* count);
+
 #ifdef __cplusplus
 }
 #endif

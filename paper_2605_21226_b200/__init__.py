@@ -105,6 +105,8 @@ def lib():
         "oq_attention_partials": ([vp, vp, C.POINTER(_Shape), vp, vp, vp, u64, u64, vp, i32, vp,
                                    sz, vp], i32),
         "oq_attention_combine": ([vp, vp, i32, i32, sz, sz, i32, vp, vp], i32),
+        "oq_timing_enable": ([i32], None),
+        "oq_timing_collect": ([C.c_char_p, C.POINTER(C.c_double), C.POINTER(i32)], i32),
     }
     for name, (args, res) in sigs.items():
         f = getattr(L, name)
@@ -135,6 +137,19 @@ def _stream(stream=None):
 
 def _ptr(t):
     return C.c_void_p(t.data_ptr())
+
+
+def timing(enable=True):
+    """Enable CUDA-event timing of the hot kernels (clears previous marks)."""
+    lib().oq_timing_enable(1 if enable else 0)
+
+
+def timing_collect(name):
+    """(total_ms, launches) of the timed launches named `name`."""
+    t = C.c_double()
+    n = C.c_int()
+    _check(lib().oq_timing_collect(name.encode(), C.byref(t), C.byref(n)))
+    return t.value, n.value
 
 
 @dataclass

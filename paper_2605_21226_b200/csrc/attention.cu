@@ -760,9 +760,7 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
   return cudaGetLastError();
 }
 
-cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecParams& pv,
-                                      const AttnArgs& a, int splits, cudaStream_t st,
-                                      int num_sms) {
+cudaError_t launch_qprep(const OqCodecParams& pk, const AttnArgs& a, cudaStream_t st) {
   const int G = a.Hq / a.Hkv, HC = (G + 7) / 8;
   QPrepParams qp;
   qp.q = a.q;
@@ -779,8 +777,13 @@ cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecPara
   qp.inv_sqrt_d = (float)pk.inv_sqrt_d;
   qp.qjl = pk.qjl;
   qprep_kernel<<<a.B * a.Hkv * HC, 256, 0, st>>>(qp);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecParams& pv,
+                                      const AttnArgs& a, int splits, cudaStream_t st,
+                                      int num_sms) {
+  const int G = a.Hq / a.Hkv, HC = (G + 7) / 8;
   const int W = 2 * pk.b_dir + pk.b_nrm;
   if (W == 10 && !pk.qjl) return launch_attn_t<10, false>(pk, a, splits, G, HC, st, num_sms);
   if (W == 10 && pk.qjl) return launch_attn_t<10, true>(pk, a, splits, G, HC, st, num_sms);

@@ -30,6 +30,30 @@ namespace {
 
 thread_local std::string g_err;
 
+// ---- optional CUDA-event timing of the hot kernels (bench.py) -------------
+// Events are recorded on the launching stream around each timed launch.
+struct KernelTimer {
+  bool on = false;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+} g_timer;
+
+struct TimedScope {
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  TimedScope(const char* n, cudaStream_t s) : name(n), st(s) {
+    if (!g_timer.on) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+  }
+  ~TimedScope() {
+    if (!a) return;
+    cudaEventRecord(b, st);
+    g_timer.marks.push_back({name, {a, b}});
+  }
+};
+
 oq_status fail(oq_status s, const std::string& msg) {
   g_err = msg;
   return s;
@@ -285,6 +309,7 @@ oq_status oq_compress(const oq_codec* c, const void* x, int dtype, size_t n, voi
   if (n && (!x || !records)) return fail(OQ_ERR_INVALID_ARGUMENT, "null buffer");
   if (dtype < OQ_DTYPE_F32 || dtype > OQ_DTYPE_BF16)
     return fail(OQ_ERR_INVALID_ARGUMENT, "unknown dtype");
+  TimedScope ts("compress", as_stream(stream));
   cudaError_t e = oqd::launch_compress(c->p, x, dtype, n, static_cast<uint8_t*>(records),
                                        as_stream(stream), c->num_sms);
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "compress kernel");
@@ -294,6 +319,7 @@ oq_status oq_decode(const oq_codec* c, const void* records, size_t n, float* out
   oq_status s = check_codec(c);
   if (s) return s;
   if (n && (!records || !out)) return fail(OQ_ERR_INVALID_ARGUMENT, "null buffer");
+  TimedScope ts("decode", as_stream(stream));
   cudaError_t e = oqd::launch_decode(c->p, static_cast<const uint8_t*>(records), n, out,
                                      as_stream(stream), c->num_sms);
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "decode kernel");
@@ -444,7 +470,12 @@ static oq_status run_partials(const oq_codec* ck, const oq_codec* cv, const oq_a
   a.partials = static_cast<float*>(ws);
   a.n_parts = n_splits;
   a.qfrag = static_cast<uint8_t*>(ws) + ((part + 255) & ~size_t(255));
-  cudaError_t e = oqd::launch_attention_partials(ck->p, cv->p, a, n_splits, st, ck->num_sms);
+  cudaError_t e = oqd::launch_qprep(ck->p, a, st);
+  if (e != cudaSuccess) return cuda_fail(e, "qprep kernel");
+  {
+    TimedScope ts("attention", st);
+    e = oqd::launch_attention_partials(ck->p, cv->p, a, n_splits, st, ck->num_sms);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "attention kernel");
   *parts_out = a.partials;
   return OQ_OK;
@@ -494,6 +525,34 @@ oq_status oq_attention_combine(const oq_codec* cv, const float* partials, int ro
   cudaError_t e = oqd::launch_attention_combine(cv->p, partials, rows, n_parts, row_stride,
                                                 part_stride, finalize, out, as_stream(stream));
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "combine kernel");
+}
+
+// Kernel timing (bench support): enable/disable, then collect the summed
+// milliseconds and launch count of every timed launch named `name`.
+void oq_timing_enable(int on) {
+  for (auto& m : g_timer.marks) {
+    cudaEventDestroy(m.second.first);
+    cudaEventDestroy(m.second.second);
+  }
+  g_timer.marks.clear();
+  g_timer.on = on != 0;
+}
+
+oq_status oq_timing_collect(const char* name, double* total_ms, int* count) {
+  double t = 0.0;
+  int n = 0;
+  for (auto& m : g_timer.marks) {
+    if (m.first != name) continue;
+    cudaError_t e = cudaEventSynchronize(m.second.second);
+    if (e != cudaSuccess) return cuda_fail(e, "event sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, m.second.first, m.second.second);
+    t += ms;
+    ++n;
+  }
+  if (total_ms) *total_ms = t;
+  if (count) *count = n;
+  return OQ_OK;
 }
 
 }  // extern "C"

@@ -42,7 +42,9 @@ bool attention_fast_path_ok(const OqCodecParams& pk, const OqCodecParams& pv);
 cudaError_t launch_pack_tiles(const OqCodecParams& p, int role, const uint8_t* recs,
                               size_t n_streams, size_t n_tokens, size_t rec_stride_tokens,
                               uint8_t* tiles, size_t tiles_cap, cudaStream_t st);
-// split-K partials over [t_begin, t_end) (K5 prologue + K3)
+// K5: query prep -> mma fragments (a.qfrag)
+cudaError_t launch_qprep(const OqCodecParams& pk, const AttnArgs& a, cudaStream_t st);
+// K3: split-K partials over [t_begin, t_end)
 cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecParams& pv,
                                       const AttnArgs& a, int splits, cudaStream_t st,
                                       int num_sms);

@@ -1,0 +1,156 @@
+"""GPU parity: K1 compress is bit-exact, K2 decode within 1e-5 (rel).
+
+The oracle (oracle/octo_oracle.c, pinned to the reference in
+test_oracle.py) is the checker; inputs are the reference's own Gaussian
+streams.  Every call goes through the C ABI (liboctoquant_b200.so).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2605_21226_b200 as oq
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+CONFIGS = [
+    dict(b_dir=3, b_nrm=1, rounding="local3x3"),
+    dict(b_dir=4, b_nrm=2, rounding="local3x3"),
+    dict(b_dir=5, b_nrm=3, rounding="local3x3"),
+    dict(b_dir=4, b_nrm=2, rounding="scalar"),
+    dict(b_dir=3, b_nrm=1, rounding="scalar"),
+    dict(b_dir=5, b_nrm=3, rounding="scalar"),
+    dict(b_dir=3, b_nrm=1, rounding="local3x3", qjl=True),
+    dict(b_dir=4, b_nrm=2, rounding="local2x2", qjl=True),
+    dict(b_dir=3, b_nrm=2, rounding="full"),
+    dict(b_dir=6, b_nrm=4, rounding="local3x3"),
+    dict(b_dir=8, b_nrm=8, rounding="local3x3", qjl=True),
+    dict(b_dir=1, b_nrm=1, rounding="local3x3"),
+    dict(dim=64, b_dir=5, b_nrm=3, rounding="local3x3"),
+    dict(dim=32, b_dir=4, b_nrm=2, rounding="local3x3", qjl=True),
+    dict(dim=16, b_dir=2, b_nrm=4, rounding="local3x3", qjl=True),
+    dict(dim=8, b_dir=3, b_nrm=3, rounding="scalar"),
+    dict(dim=4, b_dir=2, b_nrm=2, rounding="full"),
+    dict(dim=256, b_dir=4, b_nrm=2, rounding="local3x3", rotation_seed=7, qjl=True, qjl_seed=9),
+]
+
+
+def _ids(c):
+    return "-".join(f"{k}{v}" for k, v in c.items())
+
+
+def _inputs(orc, seed, n, dim):
+    x = orc.gaussian_f32(orc.L.orc_stream_child(seed, 0), n * dim).reshape(n, dim)
+    x[3] = 0.0          # zero key (codec_test.cpp:65-73)
+    x[4] *= 1e-30       # below the 1e-12 guard on ||k||
+    x[5] *= 1e20        # large norm
+    x[6] = 0.0
+    x[6, 0] = 5.0       # basis vector (codec_test.cpp:80-115)
+    return x
+
+
+@pytest.mark.parametrize("cfg", CONFIGS, ids=_ids)
+def test_compress_bit_exact_and_decode(orc, cuda, cfg):
+    import torch
+    dim = cfg.get("dim", 128)
+    n = 3000
+    x = _inputs(orc, 1, n, dim)
+    eo = orc.encoder(**cfg)
+    enc = oq.Encoder(oq.CodecConfig(**cfg))
+    assert enc.record_bytes == eo.rb
+    want = eo.encode_f32(x)
+    got = enc.compress(torch.from_numpy(x).to(cuda)).cpu().numpy()
+    bad = np.nonzero((got != want).any(1))[0]
+    assert bad.size == 0, f"{bad.size} mismatching records, first {bad[:5]}"
+    # K2 decode: rel err <= 1e-5 per vector vs the fp64 reference decode
+    dec = enc.decode(torch.from_numpy(want).to(cuda)).cpu().numpy().astype(np.float64)
+    ref = eo.decode(want)
+    num = np.linalg.norm(dec - ref, axis=1)
+    den = np.maximum(np.linalg.norm(ref, axis=1), 1e-30)
+    rel = np.where(np.linalg.norm(ref, axis=1) > 0, num / den, num)
+    assert rel.max() <= 1e-5, rel.max()
+
+
+@pytest.mark.parametrize("dtype", ["float64", "bfloat16", "float16"])
+def test_compress_other_dtypes(orc, cuda, dtype):
+    import torch
+    x = _inputs(orc, 2, 1024, 128)
+    t = torch.from_numpy(x).to(cuda).to(getattr(torch, dtype))
+    xs = t.float().cpu().numpy()  # the exact values the kernel widens
+    cfg = dict(b_dir=4, b_nrm=2)
+    got = oq.Encoder(oq.CodecConfig(**cfg)).compress(t).cpu().numpy()
+    want = orc.encoder(**cfg).encode_f32(xs)
+    assert np.array_equal(got, want)
+
+
+def test_golden_fixtures(cuda):
+    import torch
+    z = np.load(os.path.join(GOLDEN, "codes.npz"))
+    names = ["scalar", "local2x2", "local3x3", "full"]
+    for name in z.files:
+        if not name.startswith("rec_"):
+            continue
+        tag = name[4:]
+        dim, bd, bn, rnd, qjl = (int(v) for v in z["cfg_" + tag])
+        enc = oq.Encoder(oq.CodecConfig(dim=dim, b_dir=bd, b_nrm=bn, rounding=names[rnd],
+                                        qjl=bool(qjl)))
+        got = enc.compress(torch.from_numpy(z["x_" + tag]).to(cuda)).cpu().numpy()
+        assert np.array_equal(got, z[name]), tag
+
+
+@pytest.mark.parametrize("b", [2, 3, 4])
+def test_c2_million_keys_bit_exact(orc, cuda, b):
+    """BASELINE config 2: 2^20 keys, d=128, b in {4,3,2}, bit-exact vs CPU."""
+    import torch
+    n = 1 << 20
+    bd, bn = oq.default_bit_split(b)
+    g = torch.Generator(device=cuda).manual_seed(100 + b)
+    x = torch.randn((n, 128), device=cuda, generator=g, dtype=torch.float32)
+    enc = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn))
+    got = enc.compress(x).cpu().numpy()
+    want = orc.encoder(b_dir=bd, b_nrm=bn).encode_f32(x.cpu().numpy(),
+                                                     threads=os.cpu_count() or 8)
+    bad = int((got != want).any(1).sum())
+    assert bad == 0, f"{bad} of {n} records differ"
+    # decode round trip at full size: rel err <= 1e-5
+    dec = enc.decode(torch.from_numpy(want).to(cuda))
+    idx = torch.randint(0, n, (4096,), generator=torch.Generator().manual_seed(1))
+    ref = orc.encoder(b_dir=bd, b_nrm=bn).decode(want[idx.numpy()])
+    d = dec[idx.to(cuda)].cpu().numpy().astype(np.float64)
+    rel = np.linalg.norm(d - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    assert rel.max() <= 1e-5
+
+
+def test_wire_roundtrip_and_padding(orc, cuda):
+    import torch
+    cfg = oq.CodecConfig(dim=4, b_dir=3, b_nrm=1)  # 4 dir pad bits, 6 nrm pad bits
+    enc = oq.Encoder(cfg)
+    x = torch.from_numpy(_inputs(orc, 3, 64, 4)).to(cuda)
+    recs = enc.compress(x)
+    blob = oq.pack_keys(cfg, recs)
+    assert len(blob) == 20 + 64 * 7
+    cfg2, back = oq.unpack_keys(blob)
+    assert torch.equal(back.cpu(), recs.cpu())
+    # codec_test.cpp:496-517: dirty padding is rejected
+    for byte, bit in [(20 + 5, 4), (20 + 5, 7), (20 + 6, 2), (20 + 6, 7)]:
+        bad = bytearray(blob)
+        bad[byte] ^= 1 << bit
+        with pytest.raises(oq.FormatError):
+            oq.unpack_keys(bytes(bad))
+
+
+def test_pack_keys_matches_reference_blob(ref, cuda, orc):
+    import torch
+    cfg = oq.CodecConfig(b_dir=4, b_nrm=2, qjl=True)
+    x = _inputs(orc, 4, 100, 128)
+    blob = oq.pack_keys(cfg, oq.Encoder(cfg).compress(torch.from_numpy(x).to(cuda)))
+    want = ref.encoder(b_dir=4, b_nrm=2, qjl=True).encode_f32(x)
+    assert blob[20:] == want.tobytes()
+
+
+def test_rejects_dimension_mismatch(cuda):
+    import torch
+    with pytest.raises(ValueError):
+        oq.Encoder(oq.CodecConfig()).compress(torch.zeros((2, 64), device=cuda))
