@@ -280,7 +280,7 @@ def main():
     q = q_host.to(dev)
     splits = oq.default_splits(B, Hkv, Hq, T)
     stream = torch.cuda.current_stream()
-    gathered = torch.empty((world, rows, 132), dtype=torch.float32, device=dev)
+    gathered = torch.empty((world * rows, 132), dtype=torch.float32, device=dev)
     out = torch.empty((B, Hq, 128), dtype=torch.float32, device=dev)
 
     def step(qd):

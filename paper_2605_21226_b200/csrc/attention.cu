@@ -104,14 +104,13 @@ __host__ __device__ inline int v_row_dim(int g, int rho) {
 // ---------------------------------------------------------------------------
 template <int W, int N>
 __device__ __forceinline__ uint32_t code_addr(const uint32_t (&w)[N], int slot, uint32_t off) {
-  // byte offset = code * 128 + replica * 8; the table base is 2^(7+W)-aligned
-  // in the shared window, so the OR below is an ADD.
+  // shared address = table base + code * 128 + replica * 8 (off = base + 8 * replica)
   const int pos = slot * W, i = pos >> 5, sh = pos & 31;
   constexpr uint32_t M7 = ((1u << W) - 1u) << 7;
   uint32_t v;
   if (sh + W <= 32) v = sh >= 7 ? (w[i] >> (sh - 7)) : (w[i] << (7 - sh));
   else v = __funnelshift_r(w[i], w[i + 1], sh - 7);
-  return (v & M7) | off;
+  return (v & M7) + off;
 }
 
 __device__ __forceinline__ uint2 lds64(uint32_t addr) {
@@ -368,8 +367,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
 
   for (int i = tid; i < (1 << W) * 16; i += blockDim.x) tab[i] = P.tab[i >> 4];
   const uint32_t tbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
-  if (tbase & ((1u << (7 + W)) - 1u)) __trap();  // the OR-addressing needs an aligned table
-  const uint32_t toff = tbase | ((lane & 15) << 3);
+  const uint32_t toff = tbase + ((lane & 15) << 3);
   const int koff = k_block_off(W, lane), voff = v_block_off(W, lane);
   const float NEG_INF = -__int_as_float(0x7f800000);
   __syncthreads();

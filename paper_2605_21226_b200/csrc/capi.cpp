@@ -425,7 +425,8 @@ size_t oq_attention_workspace_bytes(const oq_codec* ck, const oq_codec* cv,
   if (!ck || !cv || !sh || n_splits < 1) return 0;
   const size_t rows = (size_t)sh->B * sh->Hq;
   const size_t part = rows * parts_per_row(sh, n_splits) * (4 + ck->cfg.dim) * sizeof(float);
-  const size_t qf = (size_t)sh->B * sh->Hkv * oqd::attention_qfrag_bytes(ck->p);
+  const size_t hc = sh->Hkv > 0 ? (size_t)((sh->Hq / sh->Hkv + 7) / 8) : 1;
+  const size_t qf = (size_t)sh->B * sh->Hkv * hc * oqd::attention_qfrag_bytes(ck->p);
   return ((part + 255) & ~size_t(255)) + qf + 256;
 }
 
