@@ -377,19 +377,32 @@ class KVCache:
         return (self.enc_k.tile_bytes(ROLE_K) + self.enc_v.tile_bytes(ROLE_V)) / 32.0
 
 
-def default_splits(B, Hkv, Hq, T, num_sms=148):
-    """Split-K count so that (B*Hkv*ceil(G/8)*splits) CTA work items fill the SMs evenly."""
+def default_splits(B, Hkv, Hq, T, num_sms=None):
+    """Split-K count for the persistent attention grid (one CTA per SM).
+
+    Work items = B*Hkv*ceil(G/8)*splits; pick the split count whose item
+    count is closest to a whole number of waves over the SMs (exact when
+    possible, e.g. 32 streams x 37 splits = 8 x 148), with each item at least
+    16 tiles long so its merge epilogue stays amortized."""
+    if num_sms is None:
+        try:
+            import torch
+            num_sms = torch.cuda.get_device_properties(0).multi_processor_count
+        except Exception:
+            num_sms = 148
     hc = (Hq // Hkv + 7) // 8
     streams = B * Hkv * hc
     tiles = max(1, (T + 31) // 32)
-    best = 1
-    for waves in range(1, 64):
-        s = -(-waves * num_sms // streams)
-        if s <= tiles:
-            best = s
-            if (streams * s) % num_sms == 0 or waves >= 4:
-                break
-    return max(1, min(best, tiles))
+    best, best_eff = 1, -1.0
+    for s in range(1, max(1, tiles // 16) + 1):
+        items = streams * s
+        waves = -(-items // num_sms)
+        eff = items / (waves * num_sms) - 0.002 * waves  # busy SM fraction, fewer waves
+        if eff > best_eff + 1e-9:
+            best, best_eff = s, eff
+        if waves > 16:
+            break
+    return best
 
 
 class _Workspace:

@@ -41,11 +41,17 @@ constexpr int kPartW = 132;  // (m, l, 0, 0, acc[128]): acc 16-byte aligned
 //
 // K tile (32 tokens): gamma[8][4] f32 ([g][k] = token g + 8k) | code area |
 //   [QJL: gamma_r[8][4] f16 | signs[8 g][4 c][4 k] u32 (word c of token g+8k)]
-//   code area: lane l = 4g + c owns triplets t = 11c + u (u < 11, 10 for
-//   c = 3) of tokens g + 8k (k < 4); code slot u*4 + k, W bits each,
-//   LSB-first, block padded to a word.
+//   Lane l = 4g + c owns triplets t = 11c + u (u < 11, 10 for c = 3) of
+//   tokens g + 8k (k < 4); code slot u*4 + k, W bits each, LSB-first, in a
+//   run of kw_full words (kw_3 for c = 3).
 // V tile: gamma[8][4] | code area: lane l owns triplets t = 6g + u (u < 6,
-//   1 for g = 7) of tokens v_token(c, k) (k < 8); slot u*8 + k.
+//   1 for g = 7) of tokens v_token(c, k) (k < 8); slot u*8 + k; run of
+//   vw_full words (vw_7 for g = 7).
+// The runs are stored word-interleaved so that word i of all lanes is one
+// contiguous row (a warp's i-th 4-byte load is one 128-byte line): rows
+// below the short-run length hold all 32 lanes, longer rows only the lanes
+// that own a word there (K: the 24 lanes c < 3, compacted as 3g + c; V: the
+// 28 lanes g < 7).
 __host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 __host__ __device__ inline int kw_full(int W) { return cdiv(44 * W, 32); }
 __host__ __device__ inline int kw_3(int W) { return cdiv(40 * W, 32); }
@@ -57,13 +63,14 @@ __host__ __device__ inline int ktile_bytes(int W, int qjl) {
   return (128 + 4 * kcode_words(W) + (qjl ? 64 + 512 : 0) + 15) & ~15;
 }
 __host__ __device__ inline int vtile_bytes(int W) { return (128 + 4 * vcode_words(W) + 15) & ~15; }
-__host__ __device__ inline int k_block_off(int W, int lane) {
-  const int g = lane >> 2, c = lane & 3;
-  return g * (3 * kw_full(W) + kw_3(W)) + c * kw_full(W);
+// Word offset of word i of lane l's run inside the K / V code areas.
+__host__ __device__ inline int k_word_off(int W, int lane, int i) {
+  const int g = lane >> 2, c = lane & 3, n3 = kw_3(W);
+  return i < n3 ? 32 * i + lane : 32 * n3 + 24 * (i - n3) + 3 * g + c;
 }
-__host__ __device__ inline int v_block_off(int W, int lane) {
-  const int g = lane >> 2, c = lane & 3;
-  return g < 7 ? lane * vw_full(W) : 28 * vw_full(W) + c * vw_7(W);
+__host__ __device__ inline int v_word_off(int W, int lane, int i) {
+  const int n7 = vw_7(W);
+  return i < n7 ? 32 * i + lane : 32 * n7 + 28 * (i - n7) + lane;
 }
 __host__ __device__ inline int k_token(int g, int k) { return g + 8 * k; }
 __host__ __device__ inline int v_token(int c, int k) {
@@ -187,20 +194,25 @@ struct TileRegs {
 
 template <int W, bool QJL>
 __device__ __forceinline__ void load_tile(TileRegs<W, QJL>& r, const AttnKParams& P,
-                                          size_t stream, size_t tile, int g, int c, int koff,
-                                          int voff) {
+                                          size_t stream, size_t tile, int g, int c, int kl,
+                                          int vl) {
+  // word-interleaved runs: row i of the K area is lane-indexed (kl = lane)
+  // below KW3 and compacted to 3g + c above; V rows are lane-indexed.
   using C = Cfg<W, QJL>;
   const uint8_t* kt = P.kcache + (stream * P.k_tiles_cap + tile) * (size_t)C::KTILE;
   const uint8_t* vt = P.vcache + (stream * P.v_tiles_cap + tile) * (size_t)C::VTILE;
   r.gk = __ldg(reinterpret_cast<const float4*>(kt) + g);
   r.gv = __ldg(reinterpret_cast<const float4*>(vt) + g);
-  const uint32_t* kw = reinterpret_cast<const uint32_t*>(kt + 128) + koff;
-  const uint32_t* vw = reinterpret_cast<const uint32_t*>(vt + 128) + voff;
-  const int nk = c < 3 ? C::KWF : C::KW3, nv = g < 7 ? C::VWF : C::VW7;
+  const uint32_t* kw = reinterpret_cast<const uint32_t*>(kt + 128);
+  const uint32_t* vw = reinterpret_cast<const uint32_t*>(vt + 128);
 #pragma unroll
-  for (int i = 0; i < C::KWF; ++i) r.kc[i] = i < nk ? __ldg(kw + i) : 0u;
+  for (int i = 0; i < C::KWF; ++i)
+    r.kc[i] = i < C::KW3 ? __ldg(kw + 32 * i + kl)
+                         : (c < 3 ? __ldg(kw + 32 * C::KW3 + 24 * (i - C::KW3) + 3 * g + c) : 0u);
 #pragma unroll
-  for (int i = 0; i < C::VWF; ++i) r.vc[i] = i < nv ? __ldg(vw + i) : 0u;
+  for (int i = 0; i < C::VWF; ++i)
+    r.vc[i] = i < C::VW7 ? __ldg(vw + 32 * i + vl)
+                         : (g < 7 ? __ldg(vw + 32 * C::VW7 + 28 * (i - C::VW7) + vl) : 0u);
   if (QJL) {
     const uint8_t* qa = kt + 128 + 4 * C::KCODE;
     r.gr = __ldg(reinterpret_cast<const uint2*>(qa) + g);
@@ -368,7 +380,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
   for (int i = tid; i < (1 << W) * 16; i += blockDim.x) tab[i] = P.tab[i >> 4];
   const uint32_t tbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
   const uint32_t toff = tbase + ((lane & 15) << 3);
-  const int koff = k_block_off(W, lane), voff = v_block_off(W, lane);
+  const int koff = lane, voff = lane;
   const float NEG_INF = -__int_as_float(0x7f800000);
   __syncthreads();
 
@@ -645,18 +657,13 @@ __global__ void pack_tiles_kernel(OqCodecParams p, int role, const uint8_t* __re
     for (int k = 0; k < 4; ++k)
       reinterpret_cast<float*>(out)[lane * 4 + k] = gamma_of(rec(k_token(lane, k)));
   uint32_t* codes = reinterpret_cast<uint32_t*>(out + 128);
-  // build this lane's code run
+  // build this lane's code run (word-interleaved, see the layout note)
   uint32_t acc = 0;
   int nbits = 0, wi = 0;
-  uint32_t* dst;
-  int nslots;
-  if (role == 0) {
-    dst = codes + k_block_off(W, lane);
-    nslots = (c < 3 ? 11 : 10) * 4;
-  } else {
-    dst = codes + v_block_off(W, lane);
-    nslots = (g < 7 ? 6 : 1) * 8;
-  }
+  const int nslots = role == 0 ? (c < 3 ? 11 : 10) * 4 : (g < 7 ? 6 : 1) * 8;
+  auto put = [&](int i, uint32_t w) {
+    codes[role == 0 ? k_word_off(W, lane, i) : v_word_off(W, lane, i)] = w;
+  };
   for (int slot = 0; slot < nslots; ++slot) {
     uint32_t code;
     if (role == 0) {
@@ -672,12 +679,12 @@ __global__ void pack_tiles_kernel(OqCodecParams p, int role, const uint8_t* __re
     acc |= code << nbits;
     nbits += W;
     if (nbits >= 32) {
-      dst[wi++] = acc;
+      put(wi++, acc);
       nbits -= 32;
       acc = nbits ? code >> (W - nbits) : 0u;
     }
   }
-  if (nbits) dst[wi++] = acc;
+  if (nbits) put(wi++, acc);
   if (role == 0 && p.qjl) {
     uint8_t* qa = out + 128 + 4 * kcode_words(W);
     const int sign_off = 4 + p.dir_bytes + p.nrm_bytes + 2;

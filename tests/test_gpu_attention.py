@@ -85,8 +85,10 @@ def test_split_count_does_not_change_output(orc, cuda):
     d = build(orc, cuda, B, Hq, Hkv, T, seed=5)
     q = torch.from_numpy(d["q"]).to(cuda)
     outs = [oq.attention_decode(q, d["cache"], n_splits=s).cpu().numpy() for s in (1, 3, 8, 32)]
+    # Different split counts change the running max each fp16 P operand is
+    # scaled by, so results agree to fp16 rounding (~2e-4), not bitwise.
     for o in outs[1:]:
-        assert rel_err(o, outs[0]).max() <= 1e-5
+        assert rel_err(o, outs[0]).max() <= TOL
     assert rel_err(outs[0], oracle_out(d, B, Hq, Hkv)).max() <= TOL
 
 
@@ -131,14 +133,17 @@ def test_sharded_partials_merge_like_n_splits(orc, cuda):
     out = oq.attention_combine(d["cache"].enc_v, gathered, rows, P, 132, rows * 132)
     got = out.reshape(B, Hq, 128).cpu().numpy()
     full = oq.attention_decode(q, d["cache"]).cpu().numpy()
-    assert rel_err(got, full).max() <= 1e-5
+    assert rel_err(got, full).max() <= TOL  # fp16 P rounding differs per range
     assert rel_err(got, oracle_out(d, B, Hq, Hkv, n_splits=P)).max() <= TOL
 
 
 def test_rejects_bad_shapes(orc, cuda):
+    # attention.hpp:54-56: empty cache / shape mismatch -> invalid_argument
     import torch
-    d = build(orc, cuda, 1, 7, 1, 40, seed=9)
+    d = build(orc, cuda, 1, 14, 2, 40, seed=9)
     with pytest.raises(ValueError):
         oq.attention_decode(torch.from_numpy(d["q"]).to(cuda), d["cache"], T=0)
-    with pytest.raises(ValueError):
-        oq.attention_decode(torch.from_numpy(d["q"][:, :6]).to(cuda), d["cache"])
+    with pytest.raises(ValueError):  # 7 query heads over 2 KV heads
+        oq.attention_decode(torch.from_numpy(d["q"][:, :7]).to(cuda), d["cache"])
+    with pytest.raises(ValueError):  # more tokens than the cache holds
+        oq.attention_decode(torch.from_numpy(d["q"]).to(cuda), d["cache"], T=41)

@@ -11,6 +11,9 @@ smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_o
 memcheck) timeout 600 /usr/local/cuda/bin/compute-sanitizer --tool memcheck --print-limit 20 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/memcheck.log 2>&1; echo "memcheck rc=$?" >> gpurun_out/memcheck.log;;
 pytest) timeout 1200 python -m pytest tests -m gpu -q ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log;;
 bench) timeout 600 python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log;;
+ncuattn)
+  timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:attn_partials -s 4 -c 1 -o gpurun_out/prof_attn -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-compress > gpurun_out/ncu_attn.log 2>&1; echo "ncu attn rc=$?" >> gpurun_out/ncu_attn.log
+  ;;
 ncu)
   timeout 600 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?" >> gpurun_out/ncu_launch.log
   timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:attn_partials -s 4 -c 1 -o gpurun_out/prof_attn -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-compress > gpurun_out/ncu_attn.log 2>&1; echo "ncu attn rc=$?" >> gpurun_out/ncu_attn.log
