@@ -2,7 +2,7 @@
 // OCTOPUS-compressed KV cache on sm_100a (attention.hpp:50-73 semantics, V
 // compressed with the same codec and accumulated in its rotated frame).
 //
-// Per SM, one persistent CTA of 8 warps:
+// Per SM, one persistent CTA of 12 warps:
 //   * the joint dequant table T[code] = fp16 (rho x, rho y | rho z, 0),
 //     code = ixi | ieta << b_dir | irho << 2 b_dir, sits in shared memory
 //     replicated 16x so the 16 lanes of a half-warp always hit 16 distinct
@@ -25,6 +25,7 @@
 #include <cuda_fp16.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -33,7 +34,7 @@ namespace oqd {
 
 constexpr int kTileTok = 32;
 constexpr int kNT = 43;  // triplets at dim 128
-constexpr int kAttnWarps = 8;
+constexpr int kAttnWarpsMax = 16;
 constexpr int kPartW = 132;  // (m, l, 0, 0, acc[128]): acc 16-byte aligned
 
 // ---------------------------------------------------------------------------
@@ -180,7 +181,7 @@ struct Cfg {
   static constexpr int VTILE = (128 + 4 * VCODE + 15) & ~15;
   static constexpr int QF = 18 + (QJL ? 16 : 0);
   static constexpr int TAB_BYTES = (1 << W) * 16 * 8;
-  static constexpr int SMEM = TAB_BYTES + kAttnWarps * 8 * kPartW * 4;
+  static constexpr int smem(int nw) { return TAB_BYTES + nw * 8 * kPartW * 4; }
 };
 
 template <int W, bool QJL>
@@ -247,7 +248,7 @@ __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL
 #pragma unroll
   for (int st = 0; st < 2; ++st) {
     const int k0 = 2 * st, k1 = 2 * st + 1;  // rows g, g+8 of this sub-tile
-    float d[4] = {0.f, 0.f, 0.f, 0.f};
+    float d[4] = {0.f, 0.f, 0.f, 0.f}, d2[4] = {0.f, 0.f, 0.f, 0.f};  // two MMA chains
 #pragma unroll
     for (int grp = 0; grp < 2; ++grp) {
       uint2 a[4], b[4];
@@ -258,8 +259,8 @@ __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL
       }
       const int kb = 3 * grp;
       mma16816(d, a[0].x, b[0].x, a[1].x, b[1].x, qf[2 * kb], qf[2 * kb + 1]);
-      mma16816(d, a[2].x, b[2].x, a[3].x, b[3].x, qf[2 * kb + 2], qf[2 * kb + 3]);
-      mma16816(d, __byte_perm(a[0].y, a[1].y, 0x5410), __byte_perm(b[0].y, b[1].y, 0x5410),
+      mma16816(d2, a[2].x, b[2].x, a[3].x, b[3].x, qf[2 * kb + 2], qf[2 * kb + 3]);
+      mma16816(grp ? d2 : d, __byte_perm(a[0].y, a[1].y, 0x5410), __byte_perm(b[0].y, b[1].y, 0x5410),
                __byte_perm(a[2].y, a[3].y, 0x5410), __byte_perm(b[2].y, b[3].y, 0x5410),
                qf[2 * kb + 4], qf[2 * kb + 5]);
     }
@@ -271,10 +272,12 @@ __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL
         b[r] = lds64(code_addr<W>(R.kc, (8 + r) * 4 + k1, toff));
       }
       mma16816(d, a[0].x, b[0].x, a[1].x, b[1].x, qf[12], qf[13]);
-      mma16816(d, a[2].x, b[2].x, __byte_perm(a[0].y, a[1].y, 0x5410),
+      mma16816(d2, a[2].x, b[2].x, __byte_perm(a[0].y, a[1].y, 0x5410),
                __byte_perm(b[0].y, b[1].y, 0x5410), qf[14], qf[15]);
       mma16816(d, a[2].y, b[2].y, 0u, 0u, qf[16], qf[17]);
     }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) d[i] += d2[i];
     if (QJL) {
       // residual sketch: sum_i (+-1)_i q_sketch_i on the tensor cores
       const uint32_t w0 = ~(st ? R.sg.z : R.sg.x), w1 = ~(st ? R.sg.w : R.sg.y);
@@ -368,7 +371,7 @@ __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL
   }
 }
 
-template <int W, bool QJL>
+template <int W, bool QJL, int kAttnWarps>
 __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const AttnKParams P) {
   using C = Cfg<W, QJL>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -582,29 +585,50 @@ struct CombineParams {
 };
 
 __global__ void combine_kernel(CombineParams P) {
+  // one warp per row: lanes fetch (m, l) of the parts in parallel, reduce,
+  // then every lane streams its 4 dims of each part with independent loads.
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= P.rows) return;
   const float NEG_INF = -__int_as_float(0x7f800000);
   const float* base = P.parts + (size_t)row * P.row_stride;
   float M = NEG_INF;
-  for (int i = 0; i < P.n_parts; ++i) {
-    const float* pp = base + (size_t)i * P.part_stride;
-    if (pp[1] > 0.f) M = fmaxf(M, pp[0]);
+  for (int i = lane; i < P.n_parts; i += 32) {
+    const float2 ml = *reinterpret_cast<const float2*>(base + (size_t)i * P.part_stride);
+    if (ml.y > 0.f) M = fmaxf(M, ml.x);
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
   float L = 0.f, y[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int i = 0; i < P.n_parts; ++i) {
-    const float* pp = base + (size_t)i * P.part_stride;
-    if (pp[1] > 0.f) {
-      const float f = ex2(pp[0] - M);
-      L += pp[1] * f;
-      const float4 a = *reinterpret_cast<const float4*>(pp + 4 + 4 * lane);
-      y[0] += a.x * f; y[1] += a.y * f; y[2] += a.z * f; y[3] += a.w * f;
+  for (int i0 = 0; i0 < P.n_parts; i0 += 32) {
+    // scale factor of part i0 + lane, broadcast below
+    float f = 0.f, l = 0.f;
+    if (i0 + lane < P.n_parts) {
+      const float2 ml =
+          *reinterpret_cast<const float2*>(base + (size_t)(i0 + lane) * P.part_stride);
+      if (ml.y > 0.f) {
+        f = ex2(ml.x - M);
+        l = ml.y * f;
+      }
+    }
+    float ls = l;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ls += __shfl_xor_sync(kFull, ls, o);
+    L += ls;
+    const int n = min(32, P.n_parts - i0);
+#pragma unroll 8
+    for (int j = 0; j < n; ++j) {
+      const float fj = __shfl_sync(kFull, f, j);
+      if (fj != 0.f) {
+        const float4 a4 = *reinterpret_cast<const float4*>(
+            base + (size_t)(i0 + j) * P.part_stride + 4 + 4 * lane);
+        y[0] += a4.x * fj; y[1] += a4.y * fj; y[2] += a4.z * fj; y[3] += a4.w * fj;
+      }
     }
   }
   if (!P.finalize) {
     float* o = P.out + (size_t)row * kPartW;
-    if (lane == 0) { o[0] = M; o[1] = L; o[2] = 0.f; o[3] = 0.f; }
+    if (lane == 0) *reinterpret_cast<float4*>(o) = make_float4(M, L, 0.f, 0.f);
     *reinterpret_cast<float4*>(o + 4 + 4 * lane) = make_float4(y[0], y[1], y[2], y[3]);
     return;
   }
@@ -612,13 +636,14 @@ __global__ void combine_kernel(CombineParams P) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) y[i] *= inv;
   wht128_lane4(y, lane);
-  float* o = P.out + (size_t)row * 128;
+  float r[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int e = 4 * lane + i;
     const float v = y[i] * P.inv_sqrt_d;
-    o[e] = ((P.smask[e >> 5] >> (e & 31)) & 1u) ? -v : v;
+    r[i] = ((P.smask[e >> 5] >> (e & 31)) & 1u) ? -v : v;
   }
+  *reinterpret_cast<float4*>(P.out + (size_t)row * 128 + 4 * lane) = make_float4(r[0], r[1], r[2], r[3]);
 }
 
 // ---------------------------------------------------------------------------
@@ -733,7 +758,7 @@ cudaError_t launch_pack_tiles(const OqCodecParams& p, int role, const uint8_t* r
   return cudaGetLastError();
 }
 
-template <int W, bool QJL>
+template <int W, bool QJL, int NW>
 static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int splits,
                                  int G, int HC, cudaStream_t st, int num_sms) {
   using C = Cfg<W, QJL>;
@@ -757,11 +782,11 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
   P.splits = splits;
   P.n_parts = a.n_parts;
   P.n_items = a.B * a.Hkv * HC * splits;
-  cudaError_t e = cudaFuncSetAttribute(attn_partials_kernel<W, QJL>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  cudaError_t e = cudaFuncSetAttribute(attn_partials_kernel<W, QJL, NW>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(NW));
   if (e != cudaSuccess) return e;
   const int grid = P.n_items < num_sms ? P.n_items : num_sms;
-  attn_partials_kernel<W, QJL><<<grid, kAttnWarps * 32, C::SMEM, st>>>(P);
+  attn_partials_kernel<W, QJL, NW><<<grid, NW * 32, C::smem(NW), st>>>(P);
   return cudaGetLastError();
 }
 
@@ -790,10 +815,24 @@ cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecPara
                                       int num_sms) {
   const int G = a.Hq / a.Hkv, HC = (G + 7) / 8;
   const int W = 2 * pk.b_dir + pk.b_nrm;
-  if (W == 10 && !pk.qjl) return launch_attn_t<10, false>(pk, a, splits, G, HC, st, num_sms);
-  if (W == 10 && pk.qjl) return launch_attn_t<10, true>(pk, a, splits, G, HC, st, num_sms);
-  if (W == 7 && !pk.qjl) return launch_attn_t<7, false>(pk, a, splits, G, HC, st, num_sms);
-  if (W == 7 && pk.qjl) return launch_attn_t<7, true>(pk, a, splits, G, HC, st, num_sms);
+  // Warps per CTA (one CTA per SM): OQ_ATTN_WARPS selects a variant for
+  // tuning runs; the default is the measured best.
+  static const int nw = [] {
+    const char* e = getenv("OQ_ATTN_WARPS");
+    const int v = e ? atoi(e) : 12;
+    return (v == 8 || v == 12 || v == 16) ? v : 12;
+  }();
+#define OQ_LAUNCH(WW, QQ)                                                               \
+  if (W == WW && (bool)pk.qjl == QQ) {                                                 \
+    if (nw == 8) return launch_attn_t<WW, QQ, 8>(pk, a, splits, G, HC, st, num_sms);   \
+    if (nw == 16) return launch_attn_t<WW, QQ, 16>(pk, a, splits, G, HC, st, num_sms); \
+    return launch_attn_t<WW, QQ, 12>(pk, a, splits, G, HC, st, num_sms);               \
+  }
+  OQ_LAUNCH(10, false)
+  OQ_LAUNCH(10, true)
+  OQ_LAUNCH(7, false)
+  OQ_LAUNCH(7, true)
+#undef OQ_LAUNCH
   (void)pv;
   return cudaErrorNotSupported;
 }
@@ -811,7 +850,7 @@ cudaError_t launch_attention_combine(const OqCodecParams& pv, const float* parti
   P.part_stride = part_stride;
   for (int i = 0; i < 4; ++i) P.smask[i] = pv.sign_mask[i];
   P.inv_sqrt_d = (float)pv.inv_sqrt_d;
-  const int per_block = 4;
+  const int per_block = 2;
   combine_kernel<<<(rows + per_block - 1) / per_block, 32 * per_block, 0, st>>>(P);
   return cudaGetLastError();
 }
