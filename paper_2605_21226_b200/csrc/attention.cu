@@ -110,15 +110,34 @@ __host__ __device__ inline int v_row_dim(int g, int rho) {
 }
 
 // ---------------------------------------------------------------------------
+extern __shared__ __align__(1024) uint8_t g_attn_smem[];
+
+// Shared address of the table entry for the code in `slot` of a lane's run:
+// off + code * 128, off = table base + 8 * replica.  A code inside one word
+// is masked in place (LOP3) and shifted-and-added in one LEA / LEA.HI; a
+// code straddling two words takes a funnel shift, a mask and an add.
+__device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;  // ((a * b) >> 32) + c in one IMAD.HI
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;  // a * b + c in one IMAD
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 template <int W, int N>
 __device__ __forceinline__ uint32_t code_addr(const uint32_t (&w)[N], int slot, uint32_t off) {
-  // shared address = table base + code * 128 + replica * 8 (off = base + 8 * replica)
   const int pos = slot * W, i = pos >> 5, sh = pos & 31;
-  constexpr uint32_t M7 = ((1u << W) - 1u) << 7;
-  uint32_t v;
-  if (sh + W <= 32) v = sh >= 7 ? (w[i] >> (sh - 7)) : (w[i] << (7 - sh));
-  else v = __funnelshift_r(w[i], w[i + 1], sh - 7);
-  return (v & M7) + off;
+  constexpr uint32_t M = (1u << W) - 1u;
+  if (sh + W <= 32) {
+    const uint32_t m = w[i] & (M << sh);  // LOP3
+    if (sh > 7) return mad_hi(m, 1u << (39 - sh), off);  // (m >> (sh - 7)) + off
+    return mad_lo(m, 1u << (7 - sh), off);               // (m << (7 - sh)) + off
+  }
+  const uint32_t v = __funnelshift_r(w[i], w[i + 1], sh - 7);
+  return off + (v & (M << 7));
 }
 
 __device__ __forceinline__ uint2 lds64(uint32_t addr) {
@@ -374,15 +393,15 @@ __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL
 template <int W, bool QJL, int kAttnWarps>
 __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const AttnKParams P) {
   using C = Cfg<W, QJL>;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* smem = g_attn_smem;
   uint2* tab = reinterpret_cast<uint2*>(smem);
   float* merge = reinterpret_cast<float*>(smem + C::TAB_BYTES);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, c = lane & 3;
 
   for (int i = tid; i < (1 << W) * 16; i += blockDim.x) tab[i] = P.tab[i >> 4];
-  const uint32_t tbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
-  const uint32_t toff = tbase + ((lane & 15) << 3);
+  const uint32_t toff =
+      static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + ((lane & 15) << 3);
   const int koff = lane, voff = lane;
   const float NEG_INF = -__int_as_float(0x7f800000);
   __syncthreads();
