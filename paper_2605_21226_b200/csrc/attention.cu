@@ -212,32 +212,38 @@ struct TileRegs {
   uint4 sg;
 };
 
+// Word-interleaved runs: row i of the K area is lane-indexed below KW3 and
+// compacted to 3g + c above; V rows are lane-indexed.  K and V halves load
+// separately so each can be refilled as soon as its registers are consumed.
 template <int W, bool QJL>
-__device__ __forceinline__ void load_tile(TileRegs<W, QJL>& r, const AttnKParams& P,
-                                          size_t stream, size_t tile, int g, int c, int kl,
-                                          int vl) {
-  // word-interleaved runs: row i of the K area is lane-indexed (kl = lane)
-  // below KW3 and compacted to 3g + c above; V rows are lane-indexed.
+__device__ __forceinline__ void load_k(TileRegs<W, QJL>& r, const AttnKParams& P, size_t stream,
+                                       size_t tile, int g, int c, int lane) {
   using C = Cfg<W, QJL>;
   const uint8_t* kt = P.kcache + (stream * P.k_tiles_cap + tile) * (size_t)C::KTILE;
-  const uint8_t* vt = P.vcache + (stream * P.v_tiles_cap + tile) * (size_t)C::VTILE;
   r.gk = __ldg(reinterpret_cast<const float4*>(kt) + g);
-  r.gv = __ldg(reinterpret_cast<const float4*>(vt) + g);
   const uint32_t* kw = reinterpret_cast<const uint32_t*>(kt + 128);
-  const uint32_t* vw = reinterpret_cast<const uint32_t*>(vt + 128);
 #pragma unroll
   for (int i = 0; i < C::KWF; ++i)
-    r.kc[i] = i < C::KW3 ? __ldg(kw + 32 * i + kl)
+    r.kc[i] = i < C::KW3 ? __ldg(kw + 32 * i + lane)
                          : (c < 3 ? __ldg(kw + 32 * C::KW3 + 24 * (i - C::KW3) + 3 * g + c) : 0u);
-#pragma unroll
-  for (int i = 0; i < C::VWF; ++i)
-    r.vc[i] = i < C::VW7 ? __ldg(vw + 32 * i + vl)
-                         : (g < 7 ? __ldg(vw + 32 * C::VW7 + 28 * (i - C::VW7) + vl) : 0u);
   if (QJL) {
     const uint8_t* qa = kt + 128 + 4 * C::KCODE;
     r.gr = __ldg(reinterpret_cast<const uint2*>(qa) + g);
     r.sg = __ldg(reinterpret_cast<const uint4*>(qa + 64) + (4 * g + c));
   }
+}
+
+template <int W, bool QJL>
+__device__ __forceinline__ void load_v(TileRegs<W, QJL>& r, const AttnKParams& P, size_t stream,
+                                       size_t tile, int g, int lane) {
+  using C = Cfg<W, QJL>;
+  const uint8_t* vt = P.vcache + (stream * P.v_tiles_cap + tile) * (size_t)C::VTILE;
+  r.gv = __ldg(reinterpret_cast<const float4*>(vt) + g);
+  const uint32_t* vw = reinterpret_cast<const uint32_t*>(vt + 128);
+#pragma unroll
+  for (int i = 0; i < C::VWF; ++i)
+    r.vc[i] = i < C::VW7 ? __ldg(vw + 32 * i + lane)
+                         : (g < 7 ? __ldg(vw + 32 * C::VW7 + 28 * (i - C::VW7) + lane) : 0u);
 }
 
 // Online-softmax state of one warp for its 8 heads (2 per lane).
@@ -246,11 +252,12 @@ struct WarpState {
   float m[2], l[2];
 };
 
+// QK + online softmax of one tile; returns the PV B fragments (P~^T).
 template <int W, bool QJL>
-__device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL>& R,
-                                             const uint32_t (&qf)[Cfg<W, QJL>::QF],
-                                             uint32_t toff, size_t tok0, size_t lo, size_t hi,
-                                             int g, int c) {
+__device__ __forceinline__ void qk_softmax(WarpState& S, const TileRegs<W, QJL>& R,
+                                           const uint32_t (&qf)[Cfg<W, QJL>::QF], uint32_t toff,
+                                           size_t tok0, size_t lo, size_t hi, int g, int c,
+                                           uint32_t (&pb)[2][2]) {
   const float NEG_INF = -__int_as_float(0x7f800000);
   float gk[4] = {R.gk.x, R.gk.y, R.gk.z, R.gk.w};
   float gv[4] = {R.gv.x, R.gv.y, R.gv.z, R.gv.w};
@@ -350,14 +357,18 @@ __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL
     for (int k = 0; k < 4; ++k) p[k][h] = ex2(sc[k][h] - mref);
     S.l[h] += (p[0][h] + p[1][h]) + (p[2][h] + p[3][h]);
   }
-  uint32_t pb[2][2];  // PV B fragments per 16-token sub-tile
 #pragma unroll
-  for (int st = 0; st < 2; ++st) {
+  for (int st = 0; st < 2; ++st) {  // PV B fragments per 16-token sub-tile
     pb[st][0] = movtrans(pack_h2(p[2 * st][0] * gv[2 * st], p[2 * st][1] * gv[2 * st]));
     pb[st][1] = movtrans(pack_h2(p[2 * st + 1][0] * gv[2 * st + 1], p[2 * st + 1][1] * gv[2 * st + 1]));
   }
 
-  // ---- out^T += V_hat^T P^T ------------------------------------------------
+}
+
+// out^T += V_hat^T P~^T for one tile.
+template <int W, bool QJL>
+__device__ __forceinline__ void pv_accumulate(WarpState& S, const TileRegs<W, QJL>& R,
+                                              uint32_t toff, const uint32_t (&pb)[2][2]) {
 #pragma unroll
   for (int kk = 0; kk < 2; ++kk) {
 #pragma unroll
@@ -402,7 +413,6 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
   for (int i = tid; i < (1 << W) * 16; i += blockDim.x) tab[i] = P.tab[i >> 4];
   const uint32_t toff =
       static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + ((lane & 15) << 3);
-  const int koff = lane, voff = lane;
   const float NEG_INF = -__int_as_float(0x7f800000);
   __syncthreads();
 
@@ -435,18 +445,22 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
     S.m[0] = S.m[1] = NEG_INF;
     S.l[0] = S.l[1] = 0.f;
 
-    TileRegs<W, QJL> ra, rb;
+    // One register image per warp; the K half of tile n+1 is requested as
+    // soon as QK(n) has consumed the K codes, the V half after PV(n), so
+    // each load has about half a tile of compute to land.
+    TileRegs<W, QJL> R;
     size_t tile = tlo + warp;
-    if (tile < thi) load_tile<W, QJL>(ra, P, stream, tile, g, c, koff, voff);
+    if (tile < thi) {
+      load_k<W, QJL>(R, P, stream, tile, g, c, lane);
+      load_v<W, QJL>(R, P, stream, tile, g, lane);
+    }
     while (tile < thi) {
-      size_t tn = tile + kAttnWarps;
-      if (tn < thi) load_tile<W, QJL>(rb, P, stream, tn, g, c, koff, voff);
-      process_tile<W, QJL>(S, ra, qf, toff, tile * kTileTok, lo, hi, g, c);
-      tile = tn;
-      if (tile >= thi) break;
-      tn = tile + kAttnWarps;
-      if (tn < thi) load_tile<W, QJL>(ra, P, stream, tn, g, c, koff, voff);
-      process_tile<W, QJL>(S, rb, qf, toff, tile * kTileTok, lo, hi, g, c);
+      const size_t tn = tile + kAttnWarps;
+      uint32_t pb[2][2];
+      qk_softmax<W, QJL>(S, R, qf, toff, tile * kTileTok, lo, hi, g, c, pb);
+      if (tn < thi) load_k<W, QJL>(R, P, stream, tn, g, c, lane);
+      pv_accumulate<W, QJL>(S, R, toff, pb);
+      if (tn < thi) load_v<W, QJL>(R, P, stream, tn, g, lane);
       tile = tn;
     }
 
