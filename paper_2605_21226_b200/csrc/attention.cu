@@ -212,38 +212,32 @@ struct TileRegs {
   uint4 sg;
 };
 
-// Word-interleaved runs: row i of the K area is lane-indexed below KW3 and
-// compacted to 3g + c above; V rows are lane-indexed.  K and V halves load
-// separately so each can be refilled as soon as its registers are consumed.
 template <int W, bool QJL>
-__device__ __forceinline__ void load_k(TileRegs<W, QJL>& r, const AttnKParams& P, size_t stream,
-                                       size_t tile, int g, int c, int lane) {
+__device__ __forceinline__ void load_tile(TileRegs<W, QJL>& r, const AttnKParams& P,
+                                          size_t stream, size_t tile, int g, int c, int kl,
+                                          int vl) {
+  // word-interleaved runs: row i of the K area is lane-indexed (kl = lane)
+  // below KW3 and compacted to 3g + c above; V rows are lane-indexed.
   using C = Cfg<W, QJL>;
   const uint8_t* kt = P.kcache + (stream * P.k_tiles_cap + tile) * (size_t)C::KTILE;
+  const uint8_t* vt = P.vcache + (stream * P.v_tiles_cap + tile) * (size_t)C::VTILE;
   r.gk = __ldg(reinterpret_cast<const float4*>(kt) + g);
+  r.gv = __ldg(reinterpret_cast<const float4*>(vt) + g);
   const uint32_t* kw = reinterpret_cast<const uint32_t*>(kt + 128);
+  const uint32_t* vw = reinterpret_cast<const uint32_t*>(vt + 128);
 #pragma unroll
   for (int i = 0; i < C::KWF; ++i)
-    r.kc[i] = i < C::KW3 ? __ldg(kw + 32 * i + lane)
+    r.kc[i] = i < C::KW3 ? __ldg(kw + 32 * i + kl)
                          : (c < 3 ? __ldg(kw + 32 * C::KW3 + 24 * (i - C::KW3) + 3 * g + c) : 0u);
+#pragma unroll
+  for (int i = 0; i < C::VWF; ++i)
+    r.vc[i] = i < C::VW7 ? __ldg(vw + 32 * i + vl)
+                         : (g < 7 ? __ldg(vw + 32 * C::VW7 + 28 * (i - C::VW7) + vl) : 0u);
   if (QJL) {
     const uint8_t* qa = kt + 128 + 4 * C::KCODE;
     r.gr = __ldg(reinterpret_cast<const uint2*>(qa) + g);
     r.sg = __ldg(reinterpret_cast<const uint4*>(qa + 64) + (4 * g + c));
   }
-}
-
-template <int W, bool QJL>
-__device__ __forceinline__ void load_v(TileRegs<W, QJL>& r, const AttnKParams& P, size_t stream,
-                                       size_t tile, int g, int lane) {
-  using C = Cfg<W, QJL>;
-  const uint8_t* vt = P.vcache + (stream * P.v_tiles_cap + tile) * (size_t)C::VTILE;
-  r.gv = __ldg(reinterpret_cast<const float4*>(vt) + g);
-  const uint32_t* vw = reinterpret_cast<const uint32_t*>(vt + 128);
-#pragma unroll
-  for (int i = 0; i < C::VWF; ++i)
-    r.vc[i] = i < C::VW7 ? __ldg(vw + 32 * i + lane)
-                         : (g < 7 ? __ldg(vw + 32 * C::VW7 + 28 * (i - C::VW7) + lane) : 0u);
 }
 
 // Online-softmax state of one warp for its 8 heads (2 per lane).
@@ -252,12 +246,11 @@ struct WarpState {
   float m[2], l[2];
 };
 
-// QK + online softmax of one tile; returns the PV B fragments (P~^T).
 template <int W, bool QJL>
-__device__ __forceinline__ void qk_softmax(WarpState& S, const TileRegs<W, QJL>& R,
-                                           const uint32_t (&qf)[Cfg<W, QJL>::QF], uint32_t toff,
-                                           size_t tok0, size_t lo, size_t hi, int g, int c,
-                                           uint32_t (&pb)[2][2]) {
+__device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL>& R,
+                                             const uint32_t (&qf)[Cfg<W, QJL>::QF],
+                                             uint32_t toff, size_t tok0, size_t lo, size_t hi,
+                                             int g, int c) {
   const float NEG_INF = -__int_as_float(0x7f800000);
   float gk[4] = {R.gk.x, R.gk.y, R.gk.z, R.gk.w};
   float gv[4] = {R.gv.x, R.gv.y, R.gv.z, R.gv.w};
@@ -357,18 +350,14 @@ __device__ __forceinline__ void qk_softmax(WarpState& S, const TileRegs<W, QJL>&
     for (int k = 0; k < 4; ++k) p[k][h] = ex2(sc[k][h] - mref);
     S.l[h] += (p[0][h] + p[1][h]) + (p[2][h] + p[3][h]);
   }
+  uint32_t pb[2][2];  // PV B fragments per 16-token sub-tile
 #pragma unroll
-  for (int st = 0; st < 2; ++st) {  // PV B fragments per 16-token sub-tile
+  for (int st = 0; st < 2; ++st) {
     pb[st][0] = movtrans(pack_h2(p[2 * st][0] * gv[2 * st], p[2 * st][1] * gv[2 * st]));
     pb[st][1] = movtrans(pack_h2(p[2 * st + 1][0] * gv[2 * st + 1], p[2 * st + 1][1] * gv[2 * st + 1]));
   }
 
-}
-
-// out^T += V_hat^T P~^T for one tile.
-template <int W, bool QJL>
-__device__ __forceinline__ void pv_accumulate(WarpState& S, const TileRegs<W, QJL>& R,
-                                              uint32_t toff, const uint32_t (&pb)[2][2]) {
+  // ---- out^T += V_hat^T P^T ------------------------------------------------
 #pragma unroll
   for (int kk = 0; kk < 2; ++kk) {
 #pragma unroll
@@ -401,6 +390,111 @@ __device__ __forceinline__ void pv_accumulate(WarpState& S, const TileRegs<W, QJ
   }
 }
 
+// Work item (stream, 8-head chunk, split) -> its query fragments and tiles.
+struct ItemInfo {
+  int split, sh, hc, b, kvh;
+  size_t stream, lo, hi, tlo, thi;
+};
+
+__device__ __forceinline__ ItemInfo item_info(const AttnKParams& P, int item) {
+  ItemInfo it;
+  it.split = item % P.splits;
+  it.sh = item / P.splits;  // stream * HC + hc
+  it.hc = it.sh % P.HC;
+  it.stream = it.sh / P.HC;
+  it.b = (int)(it.stream / P.Hkv);
+  it.kvh = (int)(it.stream % P.Hkv);
+  size_t len = P.T;
+  if (P.seq_lens) len = min((size_t)max(P.seq_lens[it.b], 0), P.T);
+  it.lo = P.t_begin;
+  it.hi = min(P.t_end, len);
+  it.tlo = it.thi = 0;
+  if (it.hi > it.lo) {
+    const size_t a = it.lo / kTileTok, z = (it.hi + kTileTok - 1) / kTileTok;
+    it.tlo = a + (z - a) * it.split / P.splits;
+    it.thi = a + (z - a) * (it.split + 1) / P.splits;
+  }
+  return it;
+}
+
+template <int QF>
+__device__ __forceinline__ void load_qfrag(uint32_t (&qf)[QF], const AttnKParams& P, int sh,
+                                           int lane) {
+  const uint32_t* src = P.qfrag + ((size_t)sh * 32 + lane) * QF;
+#pragma unroll
+  for (int i = 0; i < QF; ++i) qf[i] = __ldg(src + i);
+}
+
+__device__ __forceinline__ void init_state(WarpState& S) {
+  const float NEG_INF = -__int_as_float(0x7f800000);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) S.acc[i][0] = S.acc[i][1] = S.acc[i][2] = S.acc[i][3] = 0.f;
+  S.m[0] = S.m[1] = NEG_INF;
+  S.l[0] = S.l[1] = 0.f;
+}
+
+// Per-warp epilogue: reduce l over the 8 row groups and store (m, l, acc) of
+// the warp's 8 heads into its merge slot mw[8][kPartW].
+__device__ __forceinline__ void warp_state_out(WarpState& S, float* mw, int g, int c) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float v = S.l[h];
+    v += __shfl_xor_sync(kFull, v, 4);
+    v += __shfl_xor_sync(kFull, v, 8);
+    v += __shfl_xor_sync(kFull, v, 16);
+    S.l[h] = v;
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      mw[(2 * c + h) * kPartW + 0] = S.m[h];
+      mw[(2 * c + h) * kPartW + 1] = S.l[h];
+    }
+  }
+#pragma unroll
+  for (int mb = 0; mb < 9; ++mb)
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int d = v_row_dim(g, 2 * mb + half);
+      if (d >= 0) {
+        mw[(2 * c) * kPartW + 4 + d] = S.acc[mb][2 * half];
+        mw[(2 * c + 1) * kPartW + 4 + d] = S.acc[mb][2 * half + 1];
+      }
+    }
+}
+
+// CTA merge of NW warp states (SoftmaxState::merge, attention.hpp:36-44) and
+// the item's partial store; threads [0, nthreads) participate.
+template <int NW>
+__device__ __forceinline__ void merge_store(const AttnKParams& P, const ItemInfo& it,
+                                            const float* merge, int tid, int nthreads) {
+  const float NEG_INF = -__int_as_float(0x7f800000);
+  const int nh = min(8, P.G - 8 * it.hc);
+  for (int idx = tid; idx < nh * kPartW; idx += nthreads) {
+    const int h = idx / kPartW, j = idx % kPartW;
+    float M = NEG_INF;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const float* mm = merge + (w * 8 + h) * kPartW;
+      if (mm[1] > 0.f) M = fmaxf(M, mm[0]);
+    }
+    float v = 0.f;
+    if (j == 0) {
+      v = M;
+    } else if (j == 1 || j >= 4) {
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const float* mm = merge + (w * 8 + h) * kPartW;
+        if (mm[1] > 0.f) v += mm[j] * ex2(mm[0] - M);
+      }
+    }
+    const size_t row = (size_t)it.b * P.Hq + (size_t)it.kvh * P.G + 8 * it.hc + h;
+    P.partials[(row * P.n_parts + it.split) * kPartW + j] = v;
+  }
+}
+
+// Variant A: each warp streams its tiles from HBM straight into registers,
+// prefetching one tile ahead (ping-pong register images).
 template <int W, bool QJL, int kAttnWarps>
 __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const AttnKParams P) {
   using C = Cfg<W, QJL>;
@@ -413,111 +507,167 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
   for (int i = tid; i < (1 << W) * 16; i += blockDim.x) tab[i] = P.tab[i >> 4];
   const uint32_t toff =
       static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + ((lane & 15) << 3);
-  const float NEG_INF = -__int_as_float(0x7f800000);
   __syncthreads();
 
   for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-    const int split = item % P.splits;
-    const int sh = item / P.splits;  // stream * HC + hc
-    const int hc = sh % P.HC;
-    const size_t stream = sh / P.HC;
-    const int b = (int)(stream / P.Hkv), kvh = (int)(stream % P.Hkv);
-
+    const ItemInfo it = item_info(P, item);
     uint32_t qf[C::QF];
-    {
-      const uint32_t* src = P.qfrag + ((size_t)sh * 32 + lane) * C::QF;
-#pragma unroll
-      for (int i = 0; i < C::QF; ++i) qf[i] = __ldg(src + i);
-    }
-    size_t len = P.T;
-    if (P.seq_lens) len = min((size_t)max(P.seq_lens[b], 0), P.T);
-    const size_t lo = P.t_begin, hi = min(P.t_end, len);
-    size_t tlo = 0, thi = 0;
-    if (hi > lo) {
-      const size_t a = lo / kTileTok, z = (hi + kTileTok - 1) / kTileTok;
-      tlo = a + (z - a) * split / P.splits;
-      thi = a + (z - a) * (split + 1) / P.splits;
-    }
-
+    load_qfrag(qf, P, it.sh, lane);
     WarpState S;
-#pragma unroll
-    for (int i = 0; i < 9; ++i) S.acc[i][0] = S.acc[i][1] = S.acc[i][2] = S.acc[i][3] = 0.f;
-    S.m[0] = S.m[1] = NEG_INF;
-    S.l[0] = S.l[1] = 0.f;
-
-    // One register image per warp; the K half of tile n+1 is requested as
-    // soon as QK(n) has consumed the K codes, the V half after PV(n), so
-    // each load has about half a tile of compute to land.
-    TileRegs<W, QJL> R;
-    size_t tile = tlo + warp;
-    if (tile < thi) {
-      load_k<W, QJL>(R, P, stream, tile, g, c, lane);
-      load_v<W, QJL>(R, P, stream, tile, g, lane);
-    }
-    while (tile < thi) {
-      const size_t tn = tile + kAttnWarps;
-      uint32_t pb[2][2];
-      qk_softmax<W, QJL>(S, R, qf, toff, tile * kTileTok, lo, hi, g, c, pb);
-      if (tn < thi) load_k<W, QJL>(R, P, stream, tn, g, c, lane);
-      pv_accumulate<W, QJL>(S, R, toff, pb);
-      if (tn < thi) load_v<W, QJL>(R, P, stream, tn, g, lane);
+    init_state(S);
+    TileRegs<W, QJL> ra, rb;
+    size_t tile = it.tlo + warp;
+    if (tile < it.thi) load_tile<W, QJL>(ra, P, it.stream, tile, g, c, lane, lane);
+    while (tile < it.thi) {
+      size_t tn = tile + kAttnWarps;
+      if (tn < it.thi) load_tile<W, QJL>(rb, P, it.stream, tn, g, c, lane, lane);
+      process_tile<W, QJL>(S, ra, qf, toff, tile * kTileTok, it.lo, it.hi, g, c);
+      tile = tn;
+      if (tile >= it.thi) break;
+      tn = tile + kAttnWarps;
+      if (tn < it.thi) load_tile<W, QJL>(ra, P, it.stream, tn, g, c, lane, lane);
+      process_tile<W, QJL>(S, rb, qf, toff, tile * kTileTok, it.lo, it.hi, g, c);
       tile = tn;
     }
+    warp_state_out(S, merge + warp * 8 * kPartW, g, c);
+    __syncthreads();
+    merge_store<kAttnWarps>(P, it, merge, tid, blockDim.x);
+    __syncthreads();
+  }
+}
 
-    // ---- per-warp reduction of l over the 8 row groups ----------------------
+// ---------------------------------------------------------------------------
+// Variant B: TMA producer/consumer ring.  Warp NWC (the producer; one
+// elected lane) streams (K tile, V tile) pairs of the CTA's items in order
+// with cp.async.bulk into a D-stage shared-memory ring, each stage guarded by
+// a "full" mbarrier (transaction bytes) and an "empty" mbarrier (consumer
+// release).  Consumer warp w takes CTA tiles q = w, w + NWC, ...: it waits
+// on full[q % D], copies its lane's codes into registers, releases the stage
+// immediately, and runs the same QK / softmax / PV code as variant A.  The
+// ring keeps up to D tiles in flight per SM without costing registers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "OQ_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra OQ_WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+template <int W, bool QJL>
+__device__ __forceinline__ void load_tile_smem(TileRegs<W, QJL>& r, const uint8_t* kt,
+                                               const uint8_t* vt, int g, int c, int lane) {
+  using C = Cfg<W, QJL>;
+  r.gk = reinterpret_cast<const float4*>(kt)[g];
+  r.gv = reinterpret_cast<const float4*>(vt)[g];
+  const uint32_t* kw = reinterpret_cast<const uint32_t*>(kt + 128);
+  const uint32_t* vw = reinterpret_cast<const uint32_t*>(vt + 128);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float v = S.l[h];
-      v += __shfl_xor_sync(kFull, v, 4);
-      v += __shfl_xor_sync(kFull, v, 8);
-      v += __shfl_xor_sync(kFull, v, 16);
-      S.l[h] = v;
+  for (int i = 0; i < C::KWF; ++i)
+    r.kc[i] = i < C::KW3 ? kw[32 * i + lane]
+                         : (c < 3 ? kw[32 * C::KW3 + 24 * (i - C::KW3) + 3 * g + c] : 0u);
+#pragma unroll
+  for (int i = 0; i < C::VWF; ++i)
+    r.vc[i] = i < C::VW7 ? vw[32 * i + lane]
+                         : (g < 7 ? vw[32 * C::VW7 + 28 * (i - C::VW7) + lane] : 0u);
+  if (QJL) {
+    const uint8_t* qa = kt + 128 + 4 * C::KCODE;
+    r.gr = reinterpret_cast<const uint2*>(qa)[g];
+    r.sg = reinterpret_cast<const uint4*>(qa + 64)[4 * g + c];
+  }
+}
+
+template <int W, bool QJL, int NWC>
+__global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_tma_kernel(const AttnKParams P, int D) {
+  using C = Cfg<W, QJL>;
+  constexpr int STAGE = C::KTILE + C::VTILE;
+  uint8_t* smem = g_attn_smem;
+  uint2* tab = reinterpret_cast<uint2*>(smem);
+  uint8_t* ring = smem + C::TAB_BYTES;
+  float* merge = reinterpret_cast<float*>(ring + (size_t)D * STAGE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(merge + NWC * 8 * kPartW);  // full[D], empty[D]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, c = lane & 3;
+
+  for (int i = tid; i < (1 << W) * 16; i += blockDim.x) tab[i] = P.tab[i >> 4];
+  if (tid == 0) {
+    for (int i = 0; i < D; ++i) {
+      mbar_init(smem_u32(bars + i), 1);
+      mbar_init(smem_u32(bars + D + i), 1);
     }
-    float* mw = merge + warp * 8 * kPartW;
-    if (g == 0) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        mw[(2 * c + h) * kPartW + 0] = S.m[h];
-        mw[(2 * c + h) * kPartW + 1] = S.l[h];
-      }
-    }
-#pragma unroll
-    for (int mb = 0; mb < 9; ++mb)
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        const int d = v_row_dim(g, 2 * mb + half);
-        if (d >= 0) {
-          mw[(2 * c) * kPartW + 4 + d] = S.acc[mb][2 * half];
-          mw[(2 * c + 1) * kPartW + 4 + d] = S.acc[mb][2 * half + 1];
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == NWC) {  // ---- producer ------------------------------------------
+    if (lane == 0) {
+      uint32_t q = 0;
+      for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+        const ItemInfo it = item_info(P, item);
+        for (size_t t = it.tlo; t < it.thi; ++t, ++q) {
+          const uint32_t s = q % D, use = q / D;
+          if (use) mbar_wait(smem_u32(bars + D + s), (use - 1) & 1);
+          const uint32_t full = smem_u32(bars + s);
+          mbar_expect_tx(full, STAGE);
+          const uint32_t dst = smem_u32(ring + (size_t)s * STAGE);
+          bulk_g2s(dst, P.kcache + (it.stream * P.k_tiles_cap + t) * (size_t)C::KTILE, C::KTILE,
+                   full);
+          bulk_g2s(dst + C::KTILE, P.vcache + (it.stream * P.v_tiles_cap + t) * (size_t)C::VTILE,
+                   C::VTILE, full);
         }
       }
-    __syncthreads();
-    // ---- merge the 8 warps (SoftmaxState::merge, attention.hpp:36-44) -------
-    const int nh = min(8, P.G - 8 * hc);
-    for (int idx = tid; idx < nh * kPartW; idx += blockDim.x) {
-      const int h = idx / kPartW, j = idx % kPartW;
-      float M = NEG_INF;
-#pragma unroll
-      for (int w = 0; w < kAttnWarps; ++w) {
-        const float* mm = merge + (w * 8 + h) * kPartW;
-        if (mm[1] > 0.f) M = fmaxf(M, mm[0]);
-      }
-      float v = 0.f;
-      if (j == 0) {
-        v = M;
-      } else if (j == 2 || j == 3) {
-        v = 0.f;
-      } else {
-#pragma unroll
-        for (int w = 0; w < kAttnWarps; ++w) {
-          const float* mm = merge + (w * 8 + h) * kPartW;
-          if (mm[1] > 0.f) v += mm[j] * ex2(mm[0] - M);
-        }
-      }
-      const size_t row = (size_t)b * P.Hq + (size_t)kvh * P.G + 8 * hc + h;
-      P.partials[(row * P.n_parts + split) * kPartW + j] = v;
     }
-    __syncthreads();
+    return;
+  }
+
+  // ---- consumers -------------------------------------------------------------
+  const uint32_t toff = smem_u32(tab) + ((lane & 15) << 3);
+  uint32_t q0 = 0;  // CTA tile index of the current item's first tile
+  for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+    const ItemInfo it = item_info(P, item);
+    const uint32_t n = (uint32_t)(it.thi - it.tlo);
+    uint32_t qf[C::QF];
+    load_qfrag(qf, P, it.sh, lane);
+    WarpState S;
+    init_state(S);
+    for (uint32_t q = q0 + (uint32_t)((warp - (int)(q0 % NWC) + NWC) % NWC); q < q0 + n;
+         q += NWC) {
+      const uint32_t s = q % D;
+      mbar_wait(smem_u32(bars + s), (q / D) & 1);
+      TileRegs<W, QJL> R;
+      const uint8_t* st = ring + (size_t)s * STAGE;
+      load_tile_smem<W, QJL>(R, st, st + C::KTILE, g, c, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(bars + D + s));  // release (orders the reads)
+      process_tile<W, QJL>(S, R, qf, toff, (it.tlo + (q - q0)) * kTileTok, it.lo, it.hi, g, c);
+    }
+    q0 += n;
+    warp_state_out(S, merge + warp * 8 * kPartW, g, c);
+    asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");
+    merge_store<NWC>(P, it, merge, tid, NWC * 32);
+    asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");
   }
 }
 
@@ -793,7 +943,7 @@ cudaError_t launch_pack_tiles(const OqCodecParams& p, int role, const uint8_t* r
 
 template <int W, bool QJL, int NW>
 static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int splits,
-                                 int G, int HC, cudaStream_t st, int num_sms) {
+                                 int G, int HC, cudaStream_t st, int num_sms, bool tma) {
   using C = Cfg<W, QJL>;
   AttnKParams P;
   P.tab = pk.joint16;
@@ -815,10 +965,27 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
   P.splits = splits;
   P.n_parts = a.n_parts;
   P.n_items = a.B * a.Hkv * HC * splits;
+  const int grid = P.n_items < num_sms ? P.n_items : num_sms;
+  if (tma) {
+    // ring depth: whatever shared memory is left after the table and merge area
+    int max_smem = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int stage = C::KTILE + C::VTILE;
+    const int fixed = C::TAB_BYTES + NW * 8 * kPartW * 4;
+    int D = (max_smem - fixed) / (stage + 16);
+    if (D > 64) D = 64;
+    if (D < 2) return cudaErrorInvalidConfiguration;
+    const int smem = fixed + D * stage + 16 * D;
+    cudaError_t e = cudaFuncSetAttribute(attn_tma_kernel<W, QJL, NW>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attn_tma_kernel<W, QJL, NW><<<grid, (NW + 1) * 32, smem, st>>>(P, D);
+    return cudaGetLastError();
+  }
   cudaError_t e = cudaFuncSetAttribute(attn_partials_kernel<W, QJL, NW>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(NW));
   if (e != cudaSuccess) return e;
-  const int grid = P.n_items < num_sms ? P.n_items : num_sms;
   attn_partials_kernel<W, QJL, NW><<<grid, NW * 32, C::smem(NW), st>>>(P);
   return cudaGetLastError();
 }
@@ -852,14 +1019,18 @@ cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecPara
   // tuning runs; the default is the measured best.
   static const int nw = [] {
     const char* e = getenv("OQ_ATTN_WARPS");
-    const int v = e ? atoi(e) : 12;
-    return (v == 8 || v == 12 || v == 16) ? v : 12;
+    const int v = e ? atoi(e) : 8;
+    return (v == 8 || v == 12) ? v : 8;
   }();
-#define OQ_LAUNCH(WW, QQ)                                                               \
-  if (W == WW && (bool)pk.qjl == QQ) {                                                 \
-    if (nw == 8) return launch_attn_t<WW, QQ, 8>(pk, a, splits, G, HC, st, num_sms);   \
-    if (nw == 16) return launch_attn_t<WW, QQ, 16>(pk, a, splits, G, HC, st, num_sms); \
-    return launch_attn_t<WW, QQ, 12>(pk, a, splits, G, HC, st, num_sms);               \
+  // OQ_ATTN_IMPL=regs selects variant A (register prefetch); default TMA ring.
+  static const bool tma = [] {
+    const char* e = getenv("OQ_ATTN_IMPL");
+    return !(e && e[0] == 'r');
+  }();
+#define OQ_LAUNCH(WW, QQ)                                                                   \
+  if (W == WW && (bool)pk.qjl == QQ) {                                                     \
+    if (nw == 12) return launch_attn_t<WW, QQ, 12>(pk, a, splits, G, HC, st, num_sms, tma); \
+    return launch_attn_t<WW, QQ, 8>(pk, a, splits, G, HC, st, num_sms, tma);               \
   }
   OQ_LAUNCH(10, false)
   OQ_LAUNCH(10, true)
