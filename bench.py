@@ -278,7 +278,7 @@ def main():
     rows = B * Hq
     q_host = torch.randn((B, Hq, 128), generator=torch.Generator().manual_seed(99)).pin_memory()
     q = q_host.to(dev)
-    splits = oq.default_splits(B, Hkv, Hq, T)
+    splits = 0  # stream-K: equal contiguous tile ranges per SM
     stream = torch.cuda.current_stream()
     gathered = torch.empty((world * rows, 132), dtype=torch.float32, device=dev)
     out = torch.empty((B, Hq, 128), dtype=torch.float32, device=dev)

@@ -428,13 +428,15 @@ def attention_decode(q, cache: KVCache, n_splits=None, seq_lens=None, T=None, ou
                      stream=None):
     """attention_decode (attention.hpp:50-73), batched GQA over compressed K and V.
 
-    q: CUDA float32 [B, Hq, dim].  Returns [B, Hq, dim] float32.
+    q: CUDA float32 [B, Hq, dim].  Returns [B, Hq, dim] float32.  n_splits:
+    None/0 = stream-K (balanced over the SMs); k >= 1 = k contiguous chunks
+    per stream, the reference's n_splits.
     """
     import torch
     B, Hq, D = q.shape
     T = cache.tokens if T is None else T
     if n_splits is None:
-        n_splits = default_splits(B, cache.Hkv, Hq, T)
+        n_splits = 0  # stream-K: every SM gets an equal contiguous share of all tiles
     sh = _shape(cache, Hq, T, seq_lens)
     L = lib()
     ws_bytes = L.oq_attention_workspace_bytes(cache.enc_k.handle, cache.enc_v.handle,
@@ -456,7 +458,7 @@ def attention_partials(q, cache: KVCache, t_begin, t_end, n_splits=None, T=None,
     B, Hq, D = q.shape
     T = cache.tokens if T is None else T
     if n_splits is None:
-        n_splits = default_splits(B, cache.Hkv, Hq, max(1, t_end - t_begin))
+        n_splits = 0
     sh = _shape(cache, Hq, T, seq_lens)
     L = lib()
     ws_bytes = L.oq_attention_workspace_bytes(cache.enc_k.handle, cache.enc_v.handle,

@@ -189,6 +189,10 @@ struct AttnKParams {
   size_t T, t_begin, t_end;
   int B, Hq, Hkv, G, HC;
   int splits, n_parts, n_items;
+  // stream-K mode (splits == 0): the B*Hkv*HC streams x tps tiles of
+  // [tb0, tb0 + tps) are cut into gridDim.x equal contiguous ranges.
+  int streamk, n_sh;
+  size_t tb0, tps;
 };
 
 template <int W, bool QJL>
@@ -249,17 +253,19 @@ struct WarpState {
 template <int W, bool QJL>
 __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL>& R,
                                              const uint32_t (&qf)[Cfg<W, QJL>::QF],
-                                             uint32_t toff, size_t tok0, size_t lo, size_t hi,
-                                             int g, int c) {
+                                             uint32_t toff, int tok0, int lo, int hi, int g,
+                                             int c) {
   const float NEG_INF = -__int_as_float(0x7f800000);
   float gk[4] = {R.gk.x, R.gk.y, R.gk.z, R.gk.w};
   float gv[4] = {R.gv.x, R.gv.y, R.gv.z, R.gv.w};
-  bool ok[4];
+  bool ok[4] = {true, true, true, true};
+  if (tok0 < lo || tok0 + kTileTok > hi) {  // boundary tile (warp-uniform)
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const size_t t = tok0 + k_token(g, k);
-    ok[k] = t >= lo && t < hi;
-    if (!ok[k]) gk[k] = gv[k] = 0.f;
+    for (int k = 0; k < 4; ++k) {
+      const int t = tok0 + k_token(g, k);
+      ok[k] = t >= lo && t < hi;
+      if (!ok[k]) gk[k] = gv[k] = 0.f;
+    }
   }
 
   // ---- S^T = K_hat Q^T ----------------------------------------------------
@@ -390,31 +396,59 @@ __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL
   }
 }
 
-// Work item (stream, 8-head chunk, split) -> its query fragments and tiles.
-struct ItemInfo {
-  int split, sh, hc, b, kvh;
-  size_t stream, lo, hi, tlo, thi;
+// A segment: one (stream, 8-head chunk) and a tile range of it, producing
+// the partial in slot `part` of its rows.
+struct Seg {
+  int sh, hc, b, kvh, part;
+  size_t stream;
+  int lo, hi;            // valid tokens of the stream (sharding range x length)
+  size_t tlo, thi;       // tiles to process
+  bool last;             // last segment of the stream: clear the unused slots
 };
 
-__device__ __forceinline__ ItemInfo item_info(const AttnKParams& P, int item) {
-  ItemInfo it;
-  it.split = item % P.splits;
-  it.sh = item / P.splits;  // stream * HC + hc
-  it.hc = it.sh % P.HC;
-  it.stream = it.sh / P.HC;
-  it.b = (int)(it.stream / P.Hkv);
-  it.kvh = (int)(it.stream % P.Hkv);
+__device__ __forceinline__ Seg make_seg(const AttnKParams& P, int sh, size_t t0, size_t t1,
+                                        int part, bool last) {
+  Seg sg;
+  sg.sh = sh;
+  sg.hc = sh % P.HC;
+  sg.stream = sh / P.HC;
+  sg.b = (int)(sg.stream / P.Hkv);
+  sg.kvh = (int)(sg.stream % P.Hkv);
+  sg.part = part;
+  sg.last = last;
   size_t len = P.T;
-  if (P.seq_lens) len = min((size_t)max(P.seq_lens[it.b], 0), P.T);
-  it.lo = P.t_begin;
-  it.hi = min(P.t_end, len);
-  it.tlo = it.thi = 0;
-  if (it.hi > it.lo) {
-    const size_t a = it.lo / kTileTok, z = (it.hi + kTileTok - 1) / kTileTok;
-    it.tlo = a + (z - a) * it.split / P.splits;
-    it.thi = a + (z - a) * (it.split + 1) / P.splits;
+  if (P.seq_lens) len = min((size_t)max(P.seq_lens[sg.b], 0), P.T);
+  const size_t hi = min(P.t_end, len);
+  sg.lo = (int)P.t_begin;
+  sg.hi = (int)max(hi, P.t_begin);
+  // tiles wholly past this stream's valid end carry no work
+  const size_t tend = (sg.hi + kTileTok - 1) / kTileTok;
+  sg.tlo = t0;
+  sg.thi = min(t1, tend);
+  if (sg.thi < sg.tlo) sg.thi = sg.tlo;
+  return sg;
+}
+
+// Fixed split count: item -> (stream chunk, split).
+__device__ __forceinline__ Seg item_seg(const AttnKParams& P, int item) {
+  const int split = item % P.splits, sh = item / P.splits;
+  size_t len = P.T;
+  const int b = (int)((sh / P.HC) / P.Hkv);
+  if (P.seq_lens) len = min((size_t)max(P.seq_lens[b], 0), P.T);
+  const size_t hi = min(P.t_end, len);
+  size_t t0 = 0, t1 = 0;
+  if (hi > P.t_begin) {
+    const size_t a = P.t_begin / kTileTok, z = (hi + kTileTok - 1) / kTileTok;
+    t0 = a + (z - a) * split / P.splits;
+    t1 = a + (z - a) * (split + 1) / P.splits;
   }
-  return it;
+  return make_seg(P, sh, t0, t1, split, false);
+}
+
+// Stream-K: CTA boundaries over U = n_sh * tps units and the CTA owning unit x.
+__device__ __forceinline__ size_t sk_bound(size_t c, size_t U, size_t G) { return c * U / G; }
+__device__ __forceinline__ int sk_cta(size_t x, size_t U, size_t G) {
+  return (int)(((x + 1) * G - 1) / U);
 }
 
 template <int QF>
@@ -464,9 +498,9 @@ __device__ __forceinline__ void warp_state_out(WarpState& S, float* mw, int g, i
 }
 
 // CTA merge of NW warp states (SoftmaxState::merge, attention.hpp:36-44) and
-// the item's partial store; threads [0, nthreads) participate.
+// the segment's partial store; threads [0, nthreads) participate.
 template <int NW>
-__device__ __forceinline__ void merge_store(const AttnKParams& P, const ItemInfo& it,
+__device__ __forceinline__ void merge_store(const AttnKParams& P, const Seg& it,
                                             const float* merge, int tid, int nthreads) {
   const float NEG_INF = -__int_as_float(0x7f800000);
   const int nh = min(8, P.G - 8 * it.hc);
@@ -489,7 +523,10 @@ __device__ __forceinline__ void merge_store(const AttnKParams& P, const ItemInfo
       }
     }
     const size_t row = (size_t)it.b * P.Hq + (size_t)it.kvh * P.G + 8 * it.hc + h;
-    P.partials[(row * P.n_parts + it.split) * kPartW + j] = v;
+    P.partials[(row * P.n_parts + it.part) * kPartW + j] = v;
+    if (it.last && j == 1)  // slots no CTA writes for this stream: empty (l = 0)
+      for (int k = it.part + 1; k < P.n_parts; ++k)
+        P.partials[(row * P.n_parts + k) * kPartW + 1] = 0.f;
   }
 }
 
@@ -509,8 +546,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
       static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + ((lane & 15) << 3);
   __syncthreads();
 
-  for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-    const ItemInfo it = item_info(P, item);
+  auto run = [&](const Seg& it) {
     uint32_t qf[C::QF];
     load_qfrag(qf, P, it.sh, lane);
     WarpState S;
@@ -521,153 +557,31 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
     while (tile < it.thi) {
       size_t tn = tile + kAttnWarps;
       if (tn < it.thi) load_tile<W, QJL>(rb, P, it.stream, tn, g, c, lane, lane);
-      process_tile<W, QJL>(S, ra, qf, toff, tile * kTileTok, it.lo, it.hi, g, c);
+      process_tile<W, QJL>(S, ra, qf, toff, (int)(tile * kTileTok), it.lo, it.hi, g, c);
       tile = tn;
       if (tile >= it.thi) break;
       tn = tile + kAttnWarps;
       if (tn < it.thi) load_tile<W, QJL>(ra, P, it.stream, tn, g, c, lane, lane);
-      process_tile<W, QJL>(S, rb, qf, toff, tile * kTileTok, it.lo, it.hi, g, c);
+      process_tile<W, QJL>(S, rb, qf, toff, (int)(tile * kTileTok), it.lo, it.hi, g, c);
       tile = tn;
     }
     warp_state_out(S, merge + warp * 8 * kPartW, g, c);
     __syncthreads();
     merge_store<kAttnWarps>(P, it, merge, tid, blockDim.x);
     __syncthreads();
-  }
-}
+  };
 
-// ---------------------------------------------------------------------------
-// Variant B: TMA producer/consumer ring.  Warp NWC (the producer; one
-// elected lane) streams (K tile, V tile) pairs of the CTA's items in order
-// with cp.async.bulk into a D-stage shared-memory ring, each stage guarded by
-// a "full" mbarrier (transaction bytes) and an "empty" mbarrier (consumer
-// release).  Consumer warp w takes CTA tiles q = w, w + NWC, ...: it waits
-// on full[q % D], copies its lane's codes into registers, releases the stage
-// immediately, and runs the same QK / softmax / PV code as variant A.  The
-// ring keeps up to D tiles in flight per SM without costing registers.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "OQ_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra OQ_WAIT_%=;\n}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-
-template <int W, bool QJL>
-__device__ __forceinline__ void load_tile_smem(TileRegs<W, QJL>& r, const uint8_t* kt,
-                                               const uint8_t* vt, int g, int c, int lane) {
-  using C = Cfg<W, QJL>;
-  r.gk = reinterpret_cast<const float4*>(kt)[g];
-  r.gv = reinterpret_cast<const float4*>(vt)[g];
-  const uint32_t* kw = reinterpret_cast<const uint32_t*>(kt + 128);
-  const uint32_t* vw = reinterpret_cast<const uint32_t*>(vt + 128);
-#pragma unroll
-  for (int i = 0; i < C::KWF; ++i)
-    r.kc[i] = i < C::KW3 ? kw[32 * i + lane]
-                         : (c < 3 ? kw[32 * C::KW3 + 24 * (i - C::KW3) + 3 * g + c] : 0u);
-#pragma unroll
-  for (int i = 0; i < C::VWF; ++i)
-    r.vc[i] = i < C::VW7 ? vw[32 * i + lane]
-                         : (g < 7 ? vw[32 * C::VW7 + 28 * (i - C::VW7) + lane] : 0u);
-  if (QJL) {
-    const uint8_t* qa = kt + 128 + 4 * C::KCODE;
-    r.gr = reinterpret_cast<const uint2*>(qa)[g];
-    r.sg = reinterpret_cast<const uint4*>(qa + 64)[4 * g + c];
-  }
-}
-
-template <int W, bool QJL, int NWC>
-__global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_tma_kernel(const AttnKParams P, int D) {
-  using C = Cfg<W, QJL>;
-  constexpr int STAGE = C::KTILE + C::VTILE;
-  uint8_t* smem = g_attn_smem;
-  uint2* tab = reinterpret_cast<uint2*>(smem);
-  uint8_t* ring = smem + C::TAB_BYTES;
-  float* merge = reinterpret_cast<float*>(ring + (size_t)D * STAGE);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(merge + NWC * 8 * kPartW);  // full[D], empty[D]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, c = lane & 3;
-
-  for (int i = tid; i < (1 << W) * 16; i += blockDim.x) tab[i] = P.tab[i >> 4];
-  if (tid == 0) {
-    for (int i = 0; i < D; ++i) {
-      mbar_init(smem_u32(bars + i), 1);
-      mbar_init(smem_u32(bars + D + i), 1);
+  if (!P.streamk) {
+    for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) run(item_seg(P, item));
+  } else {
+    const size_t U = (size_t)P.n_sh * P.tps, G = gridDim.x;
+    const size_t u0 = sk_bound(blockIdx.x, U, G), u1 = sk_bound(blockIdx.x + 1, U, G);
+    for (size_t sh = u0 / P.tps; sh * P.tps < u1; ++sh) {
+      const size_t s0 = sh * P.tps, s1 = s0 + P.tps;
+      const size_t a = max(u0, s0), z = min(u1, s1);
+      const int part = (int)blockIdx.x - sk_cta(s0, U, G);
+      run(make_seg(P, (int)sh, P.tb0 + (a - s0), P.tb0 + (z - s0), part, z == s1));
     }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == NWC) {  // ---- producer ------------------------------------------
-    if (lane == 0) {
-      uint32_t q = 0;
-      for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-        const ItemInfo it = item_info(P, item);
-        for (size_t t = it.tlo; t < it.thi; ++t, ++q) {
-          const uint32_t s = q % D, use = q / D;
-          if (use) mbar_wait(smem_u32(bars + D + s), (use - 1) & 1);
-          const uint32_t full = smem_u32(bars + s);
-          mbar_expect_tx(full, STAGE);
-          const uint32_t dst = smem_u32(ring + (size_t)s * STAGE);
-          bulk_g2s(dst, P.kcache + (it.stream * P.k_tiles_cap + t) * (size_t)C::KTILE, C::KTILE,
-                   full);
-          bulk_g2s(dst + C::KTILE, P.vcache + (it.stream * P.v_tiles_cap + t) * (size_t)C::VTILE,
-                   C::VTILE, full);
-        }
-      }
-    }
-    return;
-  }
-
-  // ---- consumers -------------------------------------------------------------
-  const uint32_t toff = smem_u32(tab) + ((lane & 15) << 3);
-  uint32_t q0 = 0;  // CTA tile index of the current item's first tile
-  for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-    const ItemInfo it = item_info(P, item);
-    const uint32_t n = (uint32_t)(it.thi - it.tlo);
-    uint32_t qf[C::QF];
-    load_qfrag(qf, P, it.sh, lane);
-    WarpState S;
-    init_state(S);
-    for (uint32_t q = q0 + (uint32_t)((warp - (int)(q0 % NWC) + NWC) % NWC); q < q0 + n;
-         q += NWC) {
-      const uint32_t s = q % D;
-      mbar_wait(smem_u32(bars + s), (q / D) & 1);
-      TileRegs<W, QJL> R;
-      const uint8_t* st = ring + (size_t)s * STAGE;
-      load_tile_smem<W, QJL>(R, st, st + C::KTILE, g, c, lane);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(bars + D + s));  // release (orders the reads)
-      process_tile<W, QJL>(S, R, qf, toff, (it.tlo + (q - q0)) * kTileTok, it.lo, it.hi, g, c);
-    }
-    q0 += n;
-    warp_state_out(S, merge + warp * 8 * kPartW, g, c);
-    asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");
-    merge_store<NWC>(P, it, merge, tid, NWC * 32);
-    asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");
   }
 }
 
@@ -920,6 +834,19 @@ size_t attention_tile_bytes(const OqCodecParams& p, int role) {
   return role == 0 ? ktile_bytes(W, p.qjl) : vtile_bytes(W);
 }
 
+int attention_num_parts(int B, int Hq, int Hkv, uint64_t T, uint64_t t0, uint64_t t1,
+                        int n_splits, int num_sms) {
+  if (n_splits > 0) return n_splits;
+  const int G = Hq / Hkv, HC = (G + 7) / 8;
+  const uint64_t te = t1 < T ? t1 : T;
+  const uint64_t tb0 = t0 / kTileTok, tz = (te + kTileTok - 1) / kTileTok;
+  const uint64_t tps = tz > tb0 ? tz - tb0 : 0;
+  const uint64_t nsh = (uint64_t)B * Hkv * HC, U = nsh * tps;
+  const uint64_t grid = U < (uint64_t)num_sms ? (U ? U : 1) : num_sms;
+  // CTAs touching one stream: at most ceil(tps * grid / U) + 1
+  return (int)((tps * grid + U - 1) / (U ? U : 1)) + 1;
+}
+
 size_t attention_qfrag_bytes(const OqCodecParams& pk) {
   return 32 * (18 + (pk.qjl ? 16 : 0)) * 4;
 }
@@ -943,7 +870,7 @@ cudaError_t launch_pack_tiles(const OqCodecParams& p, int role, const uint8_t* r
 
 template <int W, bool QJL, int NW>
 static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int splits,
-                                 int G, int HC, cudaStream_t st, int num_sms, bool tma) {
+                                 int G, int HC, cudaStream_t st, int num_sms) {
   using C = Cfg<W, QJL>;
   AttnKParams P;
   P.tab = pk.joint16;
@@ -964,24 +891,19 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
   P.HC = HC;
   P.splits = splits;
   P.n_parts = a.n_parts;
-  P.n_items = a.B * a.Hkv * HC * splits;
-  const int grid = P.n_items < num_sms ? P.n_items : num_sms;
-  if (tma) {
-    // ring depth: whatever shared memory is left after the table and merge area
-    int max_smem = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    const int stage = C::KTILE + C::VTILE;
-    const int fixed = C::TAB_BYTES + NW * 8 * kPartW * 4;
-    int D = (max_smem - fixed) / (stage + 16);
-    if (D > 64) D = 64;
-    if (D < 2) return cudaErrorInvalidConfiguration;
-    const int smem = fixed + D * stage + 16 * D;
-    cudaError_t e = cudaFuncSetAttribute(attn_tma_kernel<W, QJL, NW>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attn_tma_kernel<W, QJL, NW><<<grid, (NW + 1) * 32, smem, st>>>(P, D);
-    return cudaGetLastError();
+  P.n_sh = a.B * a.Hkv * HC;
+  P.streamk = splits == 0;
+  P.n_items = P.n_sh * (splits > 0 ? splits : 1);
+  {
+    const size_t te = a.t_end < a.T ? a.t_end : a.T;
+    P.tb0 = a.t_begin / kTileTok;
+    const size_t tz = (te + kTileTok - 1) / kTileTok;
+    P.tps = tz > P.tb0 ? tz - P.tb0 : 0;
+  }
+  int grid = P.n_items < num_sms ? P.n_items : num_sms;
+  if (P.streamk) {
+    const size_t U = (size_t)P.n_sh * P.tps;
+    grid = (int)(U < (size_t)num_sms ? (U ? U : 1) : num_sms);
   }
   cudaError_t e = cudaFuncSetAttribute(attn_partials_kernel<W, QJL, NW>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(NW));
@@ -1022,15 +944,10 @@ cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecPara
     const int v = e ? atoi(e) : 8;
     return (v == 8 || v == 12) ? v : 8;
   }();
-  // OQ_ATTN_IMPL=regs selects variant A (register prefetch); default TMA ring.
-  static const bool tma = [] {
-    const char* e = getenv("OQ_ATTN_IMPL");
-    return !(e && e[0] == 'r');
-  }();
-#define OQ_LAUNCH(WW, QQ)                                                                   \
-  if (W == WW && (bool)pk.qjl == QQ) {                                                     \
-    if (nw == 12) return launch_attn_t<WW, QQ, 12>(pk, a, splits, G, HC, st, num_sms, tma); \
-    return launch_attn_t<WW, QQ, 8>(pk, a, splits, G, HC, st, num_sms, tma);               \
+#define OQ_LAUNCH(WW, QQ)                                                              \
+  if (W == WW && (bool)pk.qjl == QQ) {                                                \
+    if (nw == 12) return launch_attn_t<WW, QQ, 12>(pk, a, splits, G, HC, st, num_sms); \
+    return launch_attn_t<WW, QQ, 8>(pk, a, splits, G, HC, st, num_sms);               \
   }
   OQ_LAUNCH(10, false)
   OQ_LAUNCH(10, true)

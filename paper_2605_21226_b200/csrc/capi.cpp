@@ -418,13 +418,18 @@ oq_status oq_cache_pack(const oq_codec* c, int role, const void* records, uint64
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "pack tiles kernel");
 }
 
-static size_t parts_per_row(const oq_attn_shape* sh, int n_splits) { (void)sh; return (size_t)n_splits; }
+static int parts_per_row(const oq_codec* ck, const oq_attn_shape* sh, uint64_t t0, uint64_t t1,
+                         int n_splits) {
+  return oqd::attention_num_parts(sh->B, sh->Hq, sh->Hkv, sh->T, t0, t1, n_splits, ck->num_sms);
+}
 
 size_t oq_attention_workspace_bytes(const oq_codec* ck, const oq_codec* cv,
                                     const oq_attn_shape* sh, int n_splits) {
-  if (!ck || !cv || !sh || n_splits < 1) return 0;
+  if (!ck || !cv || !sh || n_splits < 0 || sh->Hkv < 1) return 0;
   const size_t rows = (size_t)sh->B * sh->Hq;
-  const size_t part = rows * parts_per_row(sh, n_splits) * (4 + ck->cfg.dim) * sizeof(float);
+  // stream-K needs the most slots for the full range; shorter ranges need fewer
+  const size_t np = (size_t)parts_per_row(ck, sh, 0, sh->T, n_splits) + 1;
+  const size_t part = rows * np * (4 + ck->cfg.dim) * sizeof(float);
   const size_t hc = sh->Hkv > 0 ? (size_t)((sh->Hq / sh->Hkv + 7) / 8) : 1;
   const size_t qf = (size_t)sh->B * sh->Hkv * hc * oqd::attention_qfrag_bytes(ck->p);
   return ((part + 255) & ~size_t(255)) + qf + 256;
@@ -440,7 +445,7 @@ static oq_status attn_check(const oq_codec* ck, const oq_codec* cv, const oq_att
     return fail(OQ_ERR_INVALID_ARGUMENT, "bad head configuration");
   if (sh->T == 0) return fail(OQ_ERR_INVALID_ARGUMENT, "empty cache");  // attention.hpp:55
   if (sh->T > sh->cap_tokens) return fail(OQ_ERR_INVALID_ARGUMENT, "values/cache length mismatch");
-  if (n_splits < 1) return fail(OQ_ERR_INVALID_ARGUMENT, "n_splits must be >= 1");
+  if (n_splits < 0) return fail(OQ_ERR_INVALID_ARGUMENT, "n_splits must be >= 0 (0 = auto)");
   if (ck->cfg.dim != cv->cfg.dim) return fail(OQ_ERR_INVALID_ARGUMENT, "K/V dim mismatch");
   if (cv->cfg.qjl) return fail(OQ_ERR_INVALID_ARGUMENT, "the V codec carries no QJL sidecar");
   if (!oqd::attention_fast_path_ok(ck->p, cv->p))
@@ -453,9 +458,11 @@ static oq_status attn_check(const oq_codec* ck, const oq_codec* cv, const oq_att
 static oq_status run_partials(const oq_codec* ck, const oq_codec* cv, const oq_attn_shape* sh,
                               const float* q, const void* kc, const void* vc, uint64_t t0,
                               uint64_t t1, int n_splits, void* ws, cudaStream_t st,
-                              float** parts_out) {
+                              float** parts_out, int* n_parts_out) {
   const size_t rows = (size_t)sh->B * sh->Hq;
-  const size_t part = rows * (size_t)n_splits * (4 + ck->cfg.dim) * sizeof(float);
+  const int np_max = parts_per_row(ck, sh, 0, sh->T, n_splits) + 1;
+  const int np = parts_per_row(ck, sh, t0, t1, n_splits);
+  const size_t part = rows * (size_t)np_max * (4 + ck->cfg.dim) * sizeof(float);
   oqd::AttnArgs a{};
   a.B = sh->B;
   a.Hq = sh->Hq;
@@ -469,7 +476,8 @@ static oq_status run_partials(const oq_codec* ck, const oq_codec* cv, const oq_a
   a.vcache = static_cast<const uint8_t*>(vc);
   a.k_tiles_cap = a.v_tiles_cap = (sh->cap_tokens + 31) / 32;
   a.partials = static_cast<float*>(ws);
-  a.n_parts = n_splits;
+  a.n_parts = np;
+  *n_parts_out = np;
   a.qfrag = static_cast<uint8_t*>(ws) + ((part + 255) & ~size_t(255));
   cudaError_t e = oqd::launch_qprep(ck->p, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "qprep kernel");
@@ -489,11 +497,12 @@ oq_status oq_attention_decode(const oq_codec* ck, const oq_codec* cv, const oq_a
   if (s) return s;
   if (!out || !ws) return fail(OQ_ERR_INVALID_ARGUMENT, "null argument");
   float* parts = nullptr;
-  s = run_partials(ck, cv, sh, q, kc, vc, 0, sh->T, n_splits, ws, as_stream(stream), &parts);
+  int np = 0;
+  s = run_partials(ck, cv, sh, q, kc, vc, 0, sh->T, n_splits, ws, as_stream(stream), &parts, &np);
   if (s) return s;
   const int rows = sh->B * sh->Hq;
   const size_t w = 4 + ck->cfg.dim;
-  cudaError_t e = oqd::launch_attention_combine(cv->p, parts, rows, n_splits, n_splits * w, w, 1,
+  cudaError_t e = oqd::launch_attention_combine(cv->p, parts, rows, np, np * w, w, 1,
                                                 out, as_stream(stream));
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "combine kernel");
 }
@@ -507,11 +516,12 @@ oq_status oq_attention_partials(const oq_codec* ck, const oq_codec* cv, const oq
   if (!partial || !ws) return fail(OQ_ERR_INVALID_ARGUMENT, "null argument");
   if (t0 > t1 || t1 > sh->T) return fail(OQ_ERR_INVALID_ARGUMENT, "bad token range");
   float* parts = nullptr;
-  s = run_partials(ck, cv, sh, q, kc, vc, t0, t1, n_splits, ws, as_stream(stream), &parts);
+  int np = 0;
+  s = run_partials(ck, cv, sh, q, kc, vc, t0, t1, n_splits, ws, as_stream(stream), &parts, &np);
   if (s) return s;
   const int rows = sh->B * sh->Hq;
   const size_t w = 4 + ck->cfg.dim;
-  cudaError_t e = oqd::launch_attention_combine(cv->p, parts, rows, n_splits, n_splits * w, w, 0,
+  cudaError_t e = oqd::launch_attention_combine(cv->p, parts, rows, np, np * w, w, 0,
                                                 partial, as_stream(stream));
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "combine kernel");
 }

@@ -37,6 +37,9 @@ struct AttnArgs {
 
 size_t attention_tile_bytes(const OqCodecParams& p, int role);  // role 0 = K, 1 = V
 size_t attention_qfrag_bytes(const OqCodecParams& pk);
+// Partial slots per (b, q head): n_splits when > 0, else the stream-K count.
+int attention_num_parts(int B, int Hq, int Hkv, uint64_t T, uint64_t t0, uint64_t t1,
+                        int n_splits, int num_sms);
 bool attention_fast_path_ok(const OqCodecParams& pk, const OqCodecParams& pv);
 // records (one (b, kv-head) stream of n tokens) -> tiles
 cudaError_t launch_pack_tiles(const OqCodecParams& p, int role, const uint8_t* recs,
