@@ -1,18 +1,25 @@
 // compress.cu — K1: fused OCTOPUS compress (Encoder::encode, codec.hpp:214-249)
 // on sm_100a, bit-exact against the fp64 CPU reference.
 //
-// Layout: LPV = max(1, D/32) lanes per vector, EPL = D/LPV contiguous
-// elements per lane, all fp64 in registers.  The rotation (signs + WHT) runs
-// in registers (in-lane butterflies for len < EPL, warp shuffles above);
-// rotated coordinates are staged once in shared memory so each lane can pick
-// up whole triplets; octahedral fold, Lloyd-Max bucketing and the joint 3x3
-// search run per lane on its triplets; the QJL epilogue re-runs the rotation
-// on the residual.  Every fp64 op is an explicitly rounded __d*_rn intrinsic
-// in the reference's evaluation order, so the codes are bit-exact (SURVEY.md
-// §7 H1).  Output is the OCTO v1 record (codec.hpp:381-393), assembled
-// byte-parallel in shared memory and stored with coalesced 32-bit writes.
-// The grid is persistent (a few CTAs per SM) so the codebook tables are
-// staged into shared memory once per CTA.
+// A CTA of 128 threads encodes VPC keys per iteration in four phases:
+//  A. rotation, LPV = max(1, D/32) lanes per key with EPL = D/LPV contiguous
+//     fp64 elements each: sequential norm, normalize, sign flips and WHT in
+//     registers (in-lane butterflies, then warp shuffles); the rotated
+//     coordinates go to shared memory;
+//  B. joint rounding, ONE THREAD PER TRIPLET over all VPC*n_tri triplets:
+//     octahedral fold and upper-bound bucketing in exact fp64; the 3x3 (or
+//     2x2 / full) window is pre-screened in fp32 and the winner is certified
+//     when it beats the runner-up by more than 1e-6 (the fp32 score error is
+//     below 3e-7 for |t| <= 1), in which case only the winner's dot product is
+//     recomputed in exact fp64 for the norm bucket; near-ties replay the
+//     reference's exact strict-'>' scan;
+//  C. (QJL) residual norm and second rotation, LPV lanes per key again;
+//  D. byte-parallel OCTO v1 record assembly (codec.hpp:381-393) in shared
+//     memory, then coalesced 32-bit stores.
+// Every fp64 op that can influence a code is an explicitly rounded __d*_rn
+// intrinsic in the reference's evaluation order, so codes are bit-exact
+// (SURVEY.md §7 H1).  The grid is persistent, so codebook tables are staged
+// into shared memory once per CTA.
 #include <cstdint>
 
 #include "common.cuh"
@@ -63,7 +70,8 @@ __device__ __forceinline__ double dot3_exact(double t0, double t1, double t2, co
 }
 
 __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const CompressSmem& s,
-                                                double t0, double t1, double t2) {
+                                                const float4* dirs32, double t0, double t1,
+                                                double t2) {
   double xi, eta;
   oct_encode_exact(t0, t1, t2, xi, eta);
   const uint32_t K = p.K;
@@ -88,8 +96,35 @@ __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const Co
     ax0 = ay0 = 0;
     ax1 = ay1 = K - 1;
   }
-  double best = -__longlong_as_double(0x7ff0000000000000ll);  // -inf
+  const double NINF = -__longlong_as_double(0x7ff0000000000000ll);
+  double best = NINF;
   uint32_t bx = ax0, by = ay0;
+  {
+    // fp32 pre-screen: |s32 - s64| < 3e-7 (|t| <= 1, unit table rows), so a
+    // winner ahead by > 1e-6 is the exact strict-'>' argmax as well.
+    const float f0 = (float)t0, f1 = (float)t1, f2 = (float)t2;
+    float b1 = -INFINITY, b2 = -INFINITY;
+    uint32_t wa = ax0, wb = ay0;
+    for (uint32_t a = ax0; a <= ax1; ++a)
+      for (uint32_t b = ay0; b <= ay1; ++b) {
+        const float4 nv = dirs32[a * K + b];
+        const float sc = fmaf(f2, nv.z, fmaf(f1, nv.y, f0 * nv.x));
+        if (sc > b1) {
+          b2 = b1;
+          b1 = sc;
+          wa = a;
+          wb = b;
+        } else if (sc > b2) {
+          b2 = sc;
+        }
+      }
+    if (b1 - b2 > 1e-6f) {  // false for NaN and exact ties
+      best = dot3_exact(t0, t1, t2, s.dirs + 3 * (wa * K + wb));
+      const double cl = best < 0.0 ? 0.0 : (best > 1.0 ? 1.0 : best);
+      const uint32_t ir = quantize_ub(s.rb, p.KR - 1, cl);
+      return wa | (wb << 8) | (ir << 16);
+    }
+  }
   for (uint32_t a = ax0; a <= ax1; ++a)
     for (uint32_t b = ay0; b <= ay1; ++b) {
       const double sc = dot3_exact(t0, t1, t2, s.dirs + 3 * (a * K + b));
@@ -177,6 +212,8 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
   const bool dirs_in_smem = kk <= 1024;
   double* dirs_s = reinterpret_cast<double*>(sp);
   if (dirs_in_smem) sp += sizeof(double) * 3 * kk;
+  float4* d32_s = reinterpret_cast<float4*>(sp);
+  if (dirs_in_smem) sp += sizeof(float4) * kk;
   float* gam_s = reinterpret_cast<float*>(sp);
   sp += sizeof(float) * S::VPC;
   uint32_t* sgn_s = reinterpret_cast<uint32_t*>(sp);  // QJL: D/32 words (>=1) per vector
@@ -194,10 +231,14 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
   for (uint32_t i = tid; i < p.K - 1; i += blockDim.x) xb_s[i] = p.xi_bnd[i];
   for (uint32_t i = tid; i < p.KR - 1; i += blockDim.x) rb_s[i] = p.rho_bnd[i];
   for (uint32_t i = tid; i < p.KR; i += blockDim.x) rc_s[i] = p.rho_c[i];
-  if (dirs_in_smem)
+  if (dirs_in_smem) {
     for (uint32_t i = tid; i < 3 * kk; i += blockDim.x) dirs_s[i] = p.dirs64[i];
+    for (uint32_t i = tid; i < kk; i += blockDim.x)
+      d32_s[i] = reinterpret_cast<const float4*>(p.dirs32)[i];
+  }
   __syncthreads();
   CompressSmem sm{xb_s, rb_s, rc_s, dirs_in_smem ? dirs_s : p.dirs64};
+  const float4* dirs32 = dirs_in_smem ? d32_s : reinterpret_cast<const float4*>(p.dirs32);
 
   const uint32_t smask = p.sign_mask[(sub * S::EPL) >> 5] >> ((sub * S::EPL) & 31);
   const uint32_t qmask = p.qsign_mask[(sub * S::EPL) >> 5] >> ((sub * S::EPL) & 31);
@@ -226,41 +267,34 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
     if (sub == S::LPV - 1)  // zero pad to 3 * n_tri (codec.hpp:229-230)
       for (int e = D; e < 3 * S::NT; ++e) ur[S::pidx(e)] = 0.0;
     if (sub == 0) gam_s[vl] = (float)gamma;  // codec.hpp:233 (double -> float RN)
-    __syncwarp();
+    __syncthreads();
 
-    // ---- per-triplet joint rounding (codec.hpp:236-241) -------------------
-    double tv[3 * S::TPL];
-    uint32_t code[S::TPL];
+    // ---- B: per-triplet joint rounding, one thread per triplet ------------
+    // (codec.hpp:236-241; QJL residual r = ur - rho n_hat, codec.hpp:243-246)
+    const int ntask = (int)min((size_t)S::VPC, n - blk * S::VPC) * S::NT;
+    for (int task = tid; task < ntask; task += blockDim.x) {
+      const int w = task / S::NT, t = task - w * S::NT;
+      double* uw = ur_s + w * S::STRIDE;
+      const double t0 = uw[S::pidx(3 * t)], t1 = uw[S::pidx(3 * t + 1)],
+                   t2 = uw[S::pidx(3 * t + 2)];
+      const uint32_t code = joint_round(p, sm, dirs32, t0, t1, t2);
+      dcode_s[w * 2 * S::NT + 2 * t] = (uint16_t)(code & 0xff);
+      dcode_s[w * 2 * S::NT + 2 * t + 1] = (uint16_t)((code >> 8) & 0xff);
+      ncode_s[w * S::NT + t] = (uint8_t)(code >> 16);
+      if (p.qjl) {
+        const uint32_t a = code & 0xff, b = (code >> 8) & 0xff, ir = code >> 16;
+        const double* nv = sm.dirs + 3 * (a * p.K + b);
+        const double r = sm.rc[ir];
+        const double tt[3] = {t0, t1, t2};
 #pragma unroll
-    for (int u = 0; u < S::TPL; ++u) {
-      const int t = sub * S::TPL + u;
-      if (t < S::NT) {
-        tv[3 * u] = ur[S::pidx(3 * t)];
-        tv[3 * u + 1] = ur[S::pidx(3 * t + 1)];
-        tv[3 * u + 2] = ur[S::pidx(3 * t + 2)];
-        code[u] = joint_round(p, sm, tv[3 * u], tv[3 * u + 1], tv[3 * u + 2]);
-        dcode_s[vl * 2 * S::NT + 2 * t] = (uint16_t)(code[u] & 0xff);
-        dcode_s[vl * 2 * S::NT + 2 * t + 1] = (uint16_t)((code[u] >> 8) & 0xff);
-        ncode_s[vl * S::NT + t] = (uint8_t)(code[u] >> 16);
+        for (int j = 0; j < 3; ++j)
+          if (3 * t + j < D) uw[S::pidx(3 * t + j)] = dsub(tt[j], dmul(r, nv[j]));
       }
     }
+    __syncthreads();
 
     if (p.qjl) {
-      // ---- QJL epilogue (codec.hpp:243-247, qjl.hpp:23-36) ------------------
-      __syncwarp();
-#pragma unroll
-      for (int u = 0; u < S::TPL; ++u) {
-        const int t = sub * S::TPL + u;
-        if (t < S::NT) {
-          const uint32_t a = code[u] & 0xff, b = (code[u] >> 8) & 0xff, ir = code[u] >> 16;
-          const double* nv = sm.dirs + 3 * (a * p.K + b);
-          const double r = sm.rc[ir];
-#pragma unroll
-          for (int j = 0; j < 3; ++j)
-            if (3 * t + j < D) ur[S::pidx(3 * t + j)] = dsub(tv[3 * u + j], dmul(r, nv[j]));
-        }
-      }
-      __syncwarp();
+      // ---- C: QJL epilogue (qjl.hpp:23-36), LPV lanes per key ---------------
 #pragma unroll
       for (int i = 0; i < S::EPL; ++i) xv[i] = ur[S::pidx(sub * S::EPL + i)];
       const double n2 = seq_sumsq<D>(xv, sub, lane);
@@ -328,7 +362,7 @@ static size_t compress_smem(const OqCodecParams& p) {
   using S = CompressShape<D>;
   const uint32_t kk = p.K * p.K;
   size_t b = sizeof(double) * S::VPC * S::STRIDE + 3 * sizeof(double) * 256;
-  if (kk <= 1024) b += sizeof(double) * 3 * kk;
+  if (kk <= 1024) b += sizeof(double) * 3 * kk + sizeof(float4) * kk;
   b += sizeof(float) * S::VPC + sizeof(uint32_t) * S::VPC * (D >= 32 ? D / 32 : 1) +
        sizeof(uint16_t) * S::VPC + sizeof(uint16_t) * S::VPC * 2 * S::NT + S::VPC * S::NT;
   b = (b + 15) & ~size_t(15);
