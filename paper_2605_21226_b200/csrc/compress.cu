@@ -47,7 +47,23 @@ struct CompressSmem {
   double* rb;
   double* rc;
   const double* dirs;
+  const uint8_t* xlut;  // 256 cells of [-1, 1]: boundaries below the cell start
+  const uint8_t* rlut;  // 256 cells of [0, 1]
 };
+
+// Exact std::upper_bound count (lloydmax.hpp:46-49) seeded by a 256-cell
+// lookup from an fp32 estimate of x; the fp64 compares that follow make the
+// result exact whatever the seed (normally one compare each way).
+__device__ __forceinline__ uint32_t quantize_lut(const double* b, uint32_t nb,
+                                                 const uint8_t* lut, double x, float lo,
+                                                 float scale) {
+  int cell = __float2int_rz(((float)x - lo) * scale);
+  cell = cell < 0 ? 0 : (cell > 255 ? 255 : cell);
+  uint32_t i = lut[cell];
+  while (i < nb && !(x < b[i])) ++i;
+  while (i > 0 && x < b[i - 1]) --i;
+  return i;
+}
 
 // ---- joint rounding of one triplet (codec.hpp:143-195) -------------------
 __device__ __forceinline__ void oct_encode_exact(double t0, double t1, double t2, double& xi,
@@ -75,12 +91,12 @@ __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const Co
   double xi, eta;
   oct_encode_exact(t0, t1, t2, xi, eta);
   const uint32_t K = p.K;
-  const uint32_t sx = quantize_ub(s.xb, K - 1, xi);
-  const uint32_t sy = quantize_ub(s.xb, K - 1, eta);
+  const uint32_t sx = quantize_lut(s.xb, K - 1, s.xlut, xi, -1.f, 128.f);
+  const uint32_t sy = quantize_lut(s.xb, K - 1, s.xlut, eta, -1.f, 128.f);
   if (p.rounding == 0) {
     double r = dsqrt(dadd(dadd(dmul(t0, t0), dmul(t1, t1)), dmul(t2, t2)));
     r = r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r);
-    const uint32_t ir = quantize_ub(s.rb, p.KR - 1, r);
+    const uint32_t ir = quantize_lut(s.rb, p.KR - 1, s.rlut, r, 0.f, 256.f);
     return sx | (sy << 8) | (ir << 16);
   }
   uint32_t ax0 = sx, ax1 = sx, ay0 = sy, ay1 = sy;
@@ -105,23 +121,34 @@ __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const Co
     const float f0 = (float)t0, f1 = (float)t1, f2 = (float)t2;
     float b1 = -INFINITY, b2 = -INFINITY;
     uint32_t wa = ax0, wb = ay0;
-    for (uint32_t a = ax0; a <= ax1; ++a)
-      for (uint32_t b = ay0; b <= ay1; ++b) {
-        const float4 nv = dirs32[a * K + b];
-        const float sc = fmaf(f2, nv.z, fmaf(f1, nv.y, f0 * nv.x));
-        if (sc > b1) {
-          b2 = b1;
-          b1 = sc;
-          wa = a;
-          wb = b;
-        } else if (sc > b2) {
-          b2 = sc;
-        }
+    auto cand = [&](uint32_t a, uint32_t b) {
+      const float4 nv = dirs32[a * K + b];
+      const float sc = fmaf(f2, nv.z, fmaf(f1, nv.y, f0 * nv.x));
+      if (sc > b1) {
+        b2 = b1;
+        b1 = sc;
+        wa = a;
+        wb = b;
+      } else if (sc > b2) {
+        b2 = sc;
       }
+    };
+    if (p.rounding == 2) {  // fixed 3x3 window, clamped cells predicated off
+#pragma unroll
+      for (int da = 0; da < 3; ++da)
+#pragma unroll
+        for (int db = 0; db < 3; ++db) {
+          const uint32_t a = sx + da - 1, b = sy + db - 1;  // wraps to huge if < 0
+          if (a < K && b < K) cand(a, b);
+        }
+    } else {
+      for (uint32_t a = ax0; a <= ax1; ++a)
+        for (uint32_t b = ay0; b <= ay1; ++b) cand(a, b);
+    }
     if (b1 - b2 > 1e-6f) {  // false for NaN and exact ties
       best = dot3_exact(t0, t1, t2, s.dirs + 3 * (wa * K + wb));
       const double cl = best < 0.0 ? 0.0 : (best > 1.0 ? 1.0 : best);
-      const uint32_t ir = quantize_ub(s.rb, p.KR - 1, cl);
+      const uint32_t ir = quantize_lut(s.rb, p.KR - 1, s.rlut, cl, 0.f, 256.f);
       return wa | (wb << 8) | (ir << 16);
     }
   }
@@ -135,8 +162,33 @@ __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const Co
       }
     }
   const double cl = best < 0.0 ? 0.0 : (best > 1.0 ? 1.0 : best);
-  const uint32_t ir = quantize_ub(s.rb, p.KR - 1, cl);
+  const uint32_t ir = quantize_lut(s.rb, p.KR - 1, s.rlut, cl, 0.f, 256.f);
   return bx | (by << 8) | (ir << 16);
+}
+
+// Vectorized row load of EPL contiguous elements, widened exactly to fp64.
+template <int EPL>
+__device__ __forceinline__ void load_row(double (&xv)[EPL], const void* x, int dtype, size_t off,
+                                         bool live) {
+  if (!live) {
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) xv[i] = 0.0;
+    return;
+  }
+  if (dtype == OQ_F32 && EPL % 4 == 0) {
+    const float4* p4 = reinterpret_cast<const float4*>(static_cast<const float*>(x) + off);
+#pragma unroll
+    for (int i = 0; i < EPL / 4; ++i) {
+      const float4 f = __ldg(p4 + i);
+      xv[4 * i] = f.x;
+      xv[4 * i + 1] = f.y;
+      xv[4 * i + 2] = f.z;
+      xv[4 * i + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) xv[i] = load_as_double(x, dtype, off + i);
+  }
 }
 
 // ---- in-register rotation: y = H (s .* x) * inv_sqrt_d (rotation.hpp:46-49)
@@ -214,6 +266,10 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
   if (dirs_in_smem) sp += sizeof(double) * 3 * kk;
   float4* d32_s = reinterpret_cast<float4*>(sp);
   if (dirs_in_smem) sp += sizeof(float4) * kk;
+  uint8_t* xlut_s = sp;
+  sp += 256;
+  uint8_t* rlut_s = sp;
+  sp += 256;
   float* gam_s = reinterpret_cast<float*>(sp);
   sp += sizeof(float) * S::VPC;
   uint32_t* sgn_s = reinterpret_cast<uint32_t*>(sp);  // QJL: D/32 words (>=1) per vector
@@ -236,8 +292,17 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
     for (uint32_t i = tid; i < kk; i += blockDim.x)
       d32_s[i] = reinterpret_cast<const float4*>(p.dirs32)[i];
   }
+  for (int c = tid; c < 256; c += blockDim.x) {
+    // number of boundaries strictly below the cell start (a seed, any value works)
+    const double x0 = -1.0 + c / 128.0, r0 = c / 256.0;
+    uint32_t i = 0, j = 0;
+    while (i < p.K - 1 && p.xi_bnd[i] < x0) ++i;
+    while (j < p.KR - 1 && p.rho_bnd[j] < r0) ++j;
+    xlut_s[c] = (uint8_t)i;
+    rlut_s[c] = (uint8_t)j;
+  }
   __syncthreads();
-  CompressSmem sm{xb_s, rb_s, rc_s, dirs_in_smem ? dirs_s : p.dirs64};
+  CompressSmem sm{xb_s, rb_s, rc_s, dirs_in_smem ? dirs_s : p.dirs64, xlut_s, rlut_s};
   const float4* dirs32 = dirs_in_smem ? d32_s : reinterpret_cast<const float4*>(p.dirs32);
 
   const uint32_t smask = p.sign_mask[(sub * S::EPL) >> 5] >> ((sub * S::EPL) & 31);
@@ -252,9 +317,7 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
 
     // ---- load, norm, normalize (codec.hpp:219-225) ------------------------
     double xv[S::EPL];
-#pragma unroll
-    for (int i = 0; i < S::EPL; ++i)
-      xv[i] = live ? load_as_double(x, dtype, v * D + sub * S::EPL + i) : 0.0;
+    load_row<S::EPL>(xv, x, dtype, v * D + sub * S::EPL, live);
     const double g2 = seq_sumsq<D>(xv, sub, lane);
     const double gamma = dsqrt(g2);
     const double inv = ddiv(1.0, gamma > 1e-12 ? gamma : 1e-12);
@@ -308,38 +371,59 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
     }
     __syncthreads();
 
-    // ---- byte-parallel OCTO record assembly (codec.hpp:381-393) -----------
+    // ---- D: OCTO record assembly (codec.hpp:381-393), word-parallel --------
+    // Each task builds one 32-bit word of a key's direction or norm bit
+    // stream (LSB-first fields, io.hpp:66-85) or its gamma / QJL bytes, then
+    // stores the word's valid bytes into the staged record.
     const size_t nv = min((size_t)S::VPC, n - blk * S::VPC);
-    const int warp = tid >> 5, nwarps = blockDim.x >> 5;
-    for (int w = warp; w < (int)nv; w += nwarps) {
-      const uint16_t* dc = dcode_s + w * 2 * S::NT;
-      const uint8_t* nc = ncode_s + w * S::NT;
-      for (uint32_t off = lane; off < rb; off += 32) {
-        uint32_t byte = 0;
-        if (off < 4) {
-          byte = (__float_as_uint(gam_s[w]) >> (8 * off)) & 0xff;
-        } else if (off < 4 + p.dir_bytes) {
-          const int j = off - 4, bd = p.b_dir;
-          const int f0 = (8 * j) / bd, f1 = min((8 * j + 7) / bd, 2 * S::NT - 1);
+    {
+      const int dw = (p.dir_bytes + 3) >> 2, nw = (p.nrm_bytes + 3) >> 2;
+      const int qw = p.qjl ? (2 + ((D + 7) >> 3) + 3) >> 2 : 0;
+      const int per = 1 + dw + nw + qw;
+      for (int task = tid; task < (int)nv * per; task += blockDim.x) {
+        const int w = task / per, k = task - w * per;
+        uint8_t* rec = stage_s + w * rb;
+        uint32_t word = 0;
+        int off, nbytes;
+        if (k == 0) {
+          word = __float_as_uint(gam_s[w]);
+          off = 0;
+          nbytes = 4;
+        } else if (k <= dw) {
+          const int wi = k - 1, bd = p.b_dir, b0 = 32 * wi;
+          const uint16_t* dc = dcode_s + w * 2 * S::NT;
+          const int f0 = b0 / bd, f1 = min((b0 + 31) / bd, 2 * S::NT - 1);
           for (int f = f0; f <= f1; ++f) {
-            const int sh = f * bd - 8 * j;
+            const int sh = f * bd - b0;
             const uint32_t c = dc[f];
-            byte |= sh >= 0 ? (c << sh) : (c >> -sh);
+            word |= sh >= 0 ? (c << sh) : (c >> -sh);
           }
-        } else if (off < 4 + p.dir_bytes + p.nrm_bytes) {
-          const int j = off - 4 - p.dir_bytes, bn = p.b_nrm;
-          const int f0 = (8 * j) / bn, f1 = min((8 * j + 7) / bn, S::NT - 1);
+          off = 4 + 4 * wi;
+          nbytes = min(4, (int)p.dir_bytes - 4 * wi);
+        } else if (k <= dw + nw) {
+          const int wi = k - 1 - dw, bn = p.b_nrm, b0 = 32 * wi;
+          const uint8_t* nc = ncode_s + w * S::NT;
+          const int f0 = b0 / bn, f1 = min((b0 + 31) / bn, S::NT - 1);
           for (int f = f0; f <= f1; ++f) {
-            const int sh = f * bn - 8 * j;
+            const int sh = f * bn - b0;
             const uint32_t c = nc[f];
-            byte |= sh >= 0 ? (c << sh) : (c >> -sh);
+            word |= sh >= 0 ? (c << sh) : (c >> -sh);
           }
-        } else {
-          const int j = off - 4 - p.dir_bytes - p.nrm_bytes;
-          if (j < 2) byte = (gr_s[w] >> (8 * j)) & 0xff;
-          else byte = (sgn_s[w * SGW + ((j - 2) >> 2)] >> (8 * ((j - 2) & 3))) & 0xff;
+          off = 4 + p.dir_bytes + 4 * wi;
+          nbytes = min(4, (int)p.nrm_bytes - 4 * wi);
+        } else {  // QJL: gamma_r u16 then the sign bytes
+          const int wi = k - 1 - dw - nw, qb = 2 + ((D + 7) >> 3);
+          for (int j = 0; j < 4 && 4 * wi + j < qb; ++j) {
+            const int byte = 4 * wi + j;
+            const uint32_t v8 = byte < 2 ? (gr_s[w] >> (8 * byte)) & 0xff
+                                         : (sgn_s[w * SGW + ((byte - 2) >> 2)] >>
+                                            (8 * ((byte - 2) & 3))) & 0xff;
+            word |= v8 << (8 * j);
+          }
+          off = 4 + p.dir_bytes + p.nrm_bytes + 4 * wi;
+          nbytes = min(4, qb - 4 * wi);
         }
-        stage_s[w * rb + off] = (uint8_t)(byte & 0xff);
+        for (int j = 0; j < nbytes; ++j) rec[off + j] = (uint8_t)(word >> (8 * j));
       }
     }
     __syncthreads();
@@ -363,6 +447,7 @@ static size_t compress_smem(const OqCodecParams& p) {
   const uint32_t kk = p.K * p.K;
   size_t b = sizeof(double) * S::VPC * S::STRIDE + 3 * sizeof(double) * 256;
   if (kk <= 1024) b += sizeof(double) * 3 * kk + sizeof(float4) * kk;
+  b += 512;
   b += sizeof(float) * S::VPC + sizeof(uint32_t) * S::VPC * (D >= 32 ? D / 32 : 1) +
        sizeof(uint16_t) * S::VPC + sizeof(uint16_t) * S::VPC * 2 * S::NT + S::VPC * S::NT;
   b = (b + 15) & ~size_t(15);
