@@ -60,9 +60,11 @@ __device__ __forceinline__ uint32_t quantize_lut(const double* b, uint32_t nb,
   int cell = __float2int_rz(((float)x - lo) * scale);
   cell = cell < 0 ? 0 : (cell > 255 ? 255 : cell);
   uint32_t i = lut[cell];
-  while (i < nb && !(x < b[i])) ++i;
-  while (i > 0 && x < b[i - 1]) --i;
-  return i;
+  i += (i < nb && !(x < b[i])) ? 1u : 0u;
+  i += (i < nb && !(x < b[i])) ? 1u : 0u;
+  i -= (i > 0 && x < b[i - 1]) ? 1u : 0u;
+  const bool ok = (i == nb || x < b[i]) && (i == 0 || !(x < b[i - 1]));
+  return ok ? i : quantize_ub(b, nb, x);  // fallback: > 2 boundaries in reach
 }
 
 // ---- joint rounding of one triplet (codec.hpp:143-195) -------------------
@@ -121,17 +123,16 @@ __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const Co
     const float f0 = (float)t0, f1 = (float)t1, f2 = (float)t2;
     float b1 = -INFINITY, b2 = -INFINITY;
     uint32_t wa = ax0, wb = ay0;
-    auto cand = [&](uint32_t a, uint32_t b) {
-      const float4 nv = dirs32[a * K + b];
-      const float sc = fmaf(f2, nv.z, fmaf(f1, nv.y, f0 * nv.x));
-      if (sc > b1) {
-        b2 = b1;
-        b1 = sc;
-        wa = a;
-        wb = b;
-      } else if (sc > b2) {
-        b2 = sc;
-      }
+    // branch-free running (best, runner-up); strict '>' keeps the first
+    // of equal fp32 scores, whose zero margin then forces the exact scan
+    auto cand = [&](uint32_t a, uint32_t b, bool valid) {
+      const float4 nv = dirs32[valid ? a * K + b : 0];
+      const float sc = valid ? fmaf(f2, nv.z, fmaf(f1, nv.y, f0 * nv.x)) : -INFINITY;
+      const bool gt = sc > b1;
+      b2 = fmaxf(b2, fminf(b1, sc));
+      b1 = fmaxf(b1, sc);
+      wa = gt ? a : wa;
+      wb = gt ? b : wb;
     };
     if (p.rounding == 2) {  // fixed 3x3 window, clamped cells predicated off
 #pragma unroll
@@ -139,11 +140,11 @@ __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const Co
 #pragma unroll
         for (int db = 0; db < 3; ++db) {
           const uint32_t a = sx + da - 1, b = sy + db - 1;  // wraps to huge if < 0
-          if (a < K && b < K) cand(a, b);
+          cand(a, b, a < K && b < K);
         }
     } else {
       for (uint32_t a = ax0; a <= ax1; ++a)
-        for (uint32_t b = ay0; b <= ay1; ++b) cand(a, b);
+        for (uint32_t b = ay0; b <= ay1; ++b) cand(a, b, true);
     }
     if (b1 - b2 > 1e-6f) {  // false for NaN and exact ties
       best = dot3_exact(t0, t1, t2, s.dirs + 3 * (wa * K + wb));
@@ -197,7 +198,10 @@ __device__ __forceinline__ void rotate_exact(double (&x)[CompressShape<D>::EPL],
                                              int sub, double scale) {
   using S = CompressShape<D>;
 #pragma unroll
-  for (int i = 0; i < S::EPL; ++i) x[i] = dflip(x[i], (smask >> i) & 1u);
+  for (int i = 0; i < S::EPL; ++i) {  // x * (+-1) is exact: XOR the sign bit
+    const uint32_t flip = (i < 31 ? smask << (31 - i) : smask >> (i - 31)) & 0x80000000u;
+    x[i] = __hiloint2double(__double2hiint(x[i]) ^ (int)flip, __double2loint(x[i]));
+  }
 #pragma unroll
   for (int len = 1; len < S::EPL; len <<= 1) {
 #pragma unroll
@@ -228,12 +232,15 @@ template <int D>
 __device__ __forceinline__ double seq_sumsq(const double (&x)[CompressShape<D>::EPL], int sub,
                                             int lane) {
   using S = CompressShape<D>;
+  double sq[S::EPL];  // exact squares in parallel; only the adds are serial
+#pragma unroll
+  for (int i = 0; i < S::EPL; ++i) sq[i] = dmul(x[i], x[i]);
   double run = 0.0;
 #pragma unroll
   for (int L = 0; L < S::LPV; ++L) {
     if (sub == L) {
 #pragma unroll
-      for (int i = 0; i < S::EPL; ++i) run = dadd(run, dmul(x[i], x[i]));
+      for (int i = 0; i < S::EPL; ++i) run = dadd(run, sq[i]);
     }
     if (S::LPV > 1) run = __shfl_sync(kFull, run, (lane & ~(S::LPV - 1)) + L);
   }
@@ -371,59 +378,45 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
     }
     __syncthreads();
 
-    // ---- D: OCTO record assembly (codec.hpp:381-393), word-parallel --------
-    // Each task builds one 32-bit word of a key's direction or norm bit
-    // stream (LSB-first fields, io.hpp:66-85) or its gamma / QJL bytes, then
-    // stores the word's valid bytes into the staged record.
+    // ---- D: OCTO record assembly (codec.hpp:381-393) ------------------------
+    // Task (key, part): part 0 writes gamma (+ the QJL bytes), part 1 the
+    // direction bit stream, part 2 the norm bit stream; each stream is packed
+    // sequentially through a 64-bit shift register (LSB-first, io.hpp:66-85).
     const size_t nv = min((size_t)S::VPC, n - blk * S::VPC);
-    {
-      const int dw = (p.dir_bytes + 3) >> 2, nw = (p.nrm_bytes + 3) >> 2;
-      const int qw = p.qjl ? (2 + ((D + 7) >> 3) + 3) >> 2 : 0;
-      const int per = 1 + dw + nw + qw;
-      for (int task = tid; task < (int)nv * per; task += blockDim.x) {
-        const int w = task / per, k = task - w * per;
-        uint8_t* rec = stage_s + w * rb;
-        uint32_t word = 0;
-        int off, nbytes;
-        if (k == 0) {
-          word = __float_as_uint(gam_s[w]);
-          off = 0;
-          nbytes = 4;
-        } else if (k <= dw) {
-          const int wi = k - 1, bd = p.b_dir, b0 = 32 * wi;
-          const uint16_t* dc = dcode_s + w * 2 * S::NT;
-          const int f0 = b0 / bd, f1 = min((b0 + 31) / bd, 2 * S::NT - 1);
-          for (int f = f0; f <= f1; ++f) {
-            const int sh = f * bd - b0;
-            const uint32_t c = dc[f];
-            word |= sh >= 0 ? (c << sh) : (c >> -sh);
-          }
-          off = 4 + 4 * wi;
-          nbytes = min(4, (int)p.dir_bytes - 4 * wi);
-        } else if (k <= dw + nw) {
-          const int wi = k - 1 - dw, bn = p.b_nrm, b0 = 32 * wi;
-          const uint8_t* nc = ncode_s + w * S::NT;
-          const int f0 = b0 / bn, f1 = min((b0 + 31) / bn, S::NT - 1);
-          for (int f = f0; f <= f1; ++f) {
-            const int sh = f * bn - b0;
-            const uint32_t c = nc[f];
-            word |= sh >= 0 ? (c << sh) : (c >> -sh);
-          }
-          off = 4 + p.dir_bytes + 4 * wi;
-          nbytes = min(4, (int)p.nrm_bytes - 4 * wi);
-        } else {  // QJL: gamma_r u16 then the sign bytes
-          const int wi = k - 1 - dw - nw, qb = 2 + ((D + 7) >> 3);
-          for (int j = 0; j < 4 && 4 * wi + j < qb; ++j) {
-            const int byte = 4 * wi + j;
-            const uint32_t v8 = byte < 2 ? (gr_s[w] >> (8 * byte)) & 0xff
-                                         : (sgn_s[w * SGW + ((byte - 2) >> 2)] >>
-                                            (8 * ((byte - 2) & 3))) & 0xff;
-            word |= v8 << (8 * j);
-          }
-          off = 4 + p.dir_bytes + p.nrm_bytes + 4 * wi;
-          nbytes = min(4, qb - 4 * wi);
+    for (int task = tid; task < 3 * (int)nv; task += blockDim.x) {
+      const int w = task / 3, part = task - 3 * w;
+      uint8_t* rec = stage_s + w * rb;
+      if (part == 0) {
+        const uint32_t gb = __float_as_uint(gam_s[w]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) rec[j] = (uint8_t)(gb >> (8 * j));
+        if (p.qjl) {
+          uint8_t* q = rec + 4 + p.dir_bytes + p.nrm_bytes;
+          q[0] = (uint8_t)gr_s[w];
+          q[1] = (uint8_t)(gr_s[w] >> 8);
+          for (int j = 0; j < ((D + 7) >> 3); ++j)
+            q[2 + j] = (uint8_t)(sgn_s[w * SGW + (j >> 2)] >> (8 * (j & 3)));
         }
-        for (int j = 0; j < nbytes; ++j) rec[off + j] = (uint8_t)(word >> (8 * j));
+      } else {
+        const bool dir = part == 1;
+        const int bits = dir ? p.b_dir : p.b_nrm, nf = dir ? 2 * S::NT : S::NT;
+        uint8_t* o = rec + (dir ? 4 : 4 + p.dir_bytes);
+        const uint16_t* dc = dcode_s + w * 2 * S::NT;
+        const uint8_t* nc = ncode_s + w * S::NT;
+        uint64_t acc = 0;
+        int nb = 0;
+        for (int f = 0; f < nf; ++f) {
+          acc |= (uint64_t)(dir ? dc[f] : nc[f]) << nb;
+          nb += bits;
+          if (nb >= 32) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = (uint8_t)(acc >> (8 * j));
+            o += 4;
+            acc >>= 32;
+            nb -= 32;
+          }
+        }
+        for (int j = 0; 8 * j < nb; ++j) o[j] = (uint8_t)(acc >> (8 * j));
       }
     }
     __syncthreads();
