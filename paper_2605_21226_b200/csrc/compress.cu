@@ -247,7 +247,9 @@ __device__ __forceinline__ double seq_sumsq(const double (&x)[CompressShape<D>::
   return run;
 }
 
-template <int D>
+// TAB: codebook tables staged in shared memory (K^2 <= 1024, i.e. b_dir <= 5);
+// otherwise they are read from global memory (L1-cached).
+template <int D, bool TAB>
 __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const void* __restrict__ x,
                                                        int dtype, size_t n,
                                                        uint8_t* __restrict__ out, int aligned) {
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
   double* rc_s = reinterpret_cast<double*>(sp);
   sp += sizeof(double) * 256;
   const uint32_t kk = p.K * p.K;
-  const bool dirs_in_smem = kk <= 1024;
+  constexpr bool dirs_in_smem = TAB;
   double* dirs_s = reinterpret_cast<double*>(sp);
   if (dirs_in_smem) sp += sizeof(double) * 3 * kk;
   float4* d32_s = reinterpret_cast<float4*>(sp);
@@ -288,7 +290,7 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
   sp += sizeof(uint16_t) * S::VPC * 2 * S::NT;
   uint8_t* ncode_s = sp;  // [VPC][NT]
   sp += S::VPC * S::NT;
-  sp = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sp) + 15) & ~uintptr_t(15));
+  sp = smem_raw + (((sp - smem_raw) + 15) & ~15);  // keep the shared address space
   uint8_t* stage_s = sp;  // [VPC * rec_bytes]
 
   for (uint32_t i = tid; i < p.K - 1; i += blockDim.x) xb_s[i] = p.xi_bnd[i];
@@ -309,8 +311,13 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
     rlut_s[c] = (uint8_t)j;
   }
   __syncthreads();
-  CompressSmem sm{xb_s, rb_s, rc_s, dirs_in_smem ? dirs_s : p.dirs64, xlut_s, rlut_s};
-  const float4* dirs32 = dirs_in_smem ? d32_s : reinterpret_cast<const float4*>(p.dirs32);
+  const double* dirs64 = dirs_s;
+  const float4* dirs32 = d32_s;
+  if constexpr (!TAB) {
+    dirs64 = p.dirs64;
+    dirs32 = reinterpret_cast<const float4*>(p.dirs32);
+  }
+  CompressSmem sm{xb_s, rb_s, rc_s, dirs64, xlut_s, rlut_s};
 
   const uint32_t smask = p.sign_mask[(sub * S::EPL) >> 5] >> ((sub * S::EPL) & 31);
   const uint32_t qmask = p.qsign_mask[(sub * S::EPL) >> 5] >> ((sub * S::EPL) & 31);
@@ -405,8 +412,8 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
         const uint8_t* nc = ncode_s + w * S::NT;
         uint64_t acc = 0;
         int nb = 0;
-        for (int f = 0; f < nf; ++f) {
-          acc |= (uint64_t)(dir ? dc[f] : nc[f]) << nb;
+        auto push = [&](uint32_t code) {
+          acc |= (uint64_t)code << nb;
           nb += bits;
           if (nb >= 32) {
 #pragma unroll
@@ -415,7 +422,11 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
             acc >>= 32;
             nb -= 32;
           }
-        }
+        };
+        if (dir)
+          for (int f = 0; f < nf; ++f) push(dc[f]);
+        else
+          for (int f = 0; f < nf; ++f) push(nc[f]);
         for (int j = 0; 8 * j < nb; ++j) o[j] = (uint8_t)(acc >> (8 * j));
       }
     }
@@ -448,24 +459,31 @@ static size_t compress_smem(const OqCodecParams& p) {
   return b;
 }
 
-template <int D>
-static cudaError_t launch_compress_d(const OqCodecParams& p, const void* x, int dtype, size_t n,
+template <int D, bool TAB>
+static cudaError_t launch_compress_dt(const OqCodecParams& p, const void* x, int dtype, size_t n,
                                      uint8_t* out, cudaStream_t st, int num_sms) {
   using S = CompressShape<D>;
   const size_t smem = compress_smem<D>(p);
-  cudaError_t e = cudaFuncSetAttribute(compress_kernel<D>,
+  cudaError_t e = cudaFuncSetAttribute(compress_kernel<D, TAB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compress_kernel<D>, S::THREADS, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compress_kernel<D, TAB>, S::THREADS, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const size_t nblocks = (n + S::VPC - 1) / S::VPC;
   size_t grid = (size_t)per_sm * num_sms;
   if (grid > nblocks) grid = nblocks;
   const int aligned = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
-  compress_kernel<D><<<(unsigned)grid, S::THREADS, smem, st>>>(p, x, dtype, n, out, aligned);
+  compress_kernel<D, TAB><<<(unsigned)grid, S::THREADS, smem, st>>>(p, x, dtype, n, out, aligned);
   return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_compress_d(const OqCodecParams& p, const void* x, int dtype, size_t n,
+                                     uint8_t* out, cudaStream_t st, int num_sms) {
+  return p.K * p.K <= 1024 ? launch_compress_dt<D, true>(p, x, dtype, n, out, st, num_sms)
+                           : launch_compress_dt<D, false>(p, x, dtype, n, out, st, num_sms);
 }
 
 cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, size_t n,
