@@ -102,6 +102,26 @@ oq_status upload(oq_codec* c, const std::vector<T>& h, const T** out) {
   return OQ_OK;
 }
 
+// Index brackets for quantize (compress.cu quantize_lut): cell c of [lo, hi]
+// stores lo | hi << 16 with every boundary < cell_start - 1e-6 counted in lo
+// and every boundary <= cell_end + 1e-6 counted in hi.
+std::vector<uint32_t> bracket_lut(const std::vector<double>& b, double lo, double hi) {
+  std::vector<uint32_t> lut(1024);
+  const double w = (hi - lo) / 1024.0;
+  for (int c = 0; c < 1024; ++c) {
+    const double x0 = lo + c * w - 1e-6, x1 = lo + (c + 1) * w + 1e-6;
+    uint32_t l = 0, h = 0;
+    for (double v : b) {
+      l += v < x0 ? 1u : 0u;
+      h += v <= x1 ? 1u : 0u;
+    }
+    if (c == 1023) h = (uint32_t)b.size();  // x clamped into the last cell
+    if (c == 0) l = 0;
+    lut[c] = l | (h << 16);
+  }
+  return lut;
+}
+
 uint16_t half_bits(double v) {
   const __half h = __double2half(v);
   uint16_t b;
@@ -175,7 +195,9 @@ oq_status build_codec(const oq_config* cfg, const oqh::Book& xi, const oqh::Book
   if ((s = upload(c, xi.boundaries, &p.xi_bnd)) || (s = upload(c, rho.boundaries, &p.rho_bnd)) ||
       (s = upload(c, rho.centroids, &p.rho_c)) || (s = upload(c, dirs64, &p.dirs64)) ||
       (s = upload(c, dirs32, &p.dirs32)) || (s = upload(c, rho32, &p.rho32)) ||
-      (s = upload(c, joint, &p.joint16))) {
+      (s = upload(c, joint, &p.joint16)) ||
+      (s = upload(c, bracket_lut(xi.boundaries, -1.0, 1.0), &p.xi_lut)) ||
+      (s = upload(c, bracket_lut(rho.boundaries, 0.0, 1.0), &p.rho_lut))) {
     oq_codec_destroy(c);
     return s;
   }

@@ -26,4 +26,6 @@ struct OqCodecParams {
   const float* dirs32;     // K*K*4 fp32 copy (x, y, z, 0)
   const float* rho32;      // KR fp32 centroids
   const uint2* joint16;    // 2^(2 b_dir + b_nrm) fp16 (rho*x, rho*y | rho*z, 0)
+  const uint32_t* xi_lut;  // 1024-cell index brackets over [-1, 1] (compress quantize)
+  const uint32_t* rho_lut; // 1024-cell index brackets over [0, 1]
 };

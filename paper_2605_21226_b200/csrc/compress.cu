@@ -47,27 +47,25 @@ struct CompressSmem {
   double* rb;
   double* rc;
   const double* dirs;
-  const uint8_t* xlut;  // 256 cells of [-1, 1]: boundaries below the cell start
-  const uint8_t* rlut;  // 256 cells of [0, 1]
+  const uint32_t* xlut;  // 1024 cells of [-1, 1]: (lo | hi << 16) index bracket
+  const uint32_t* rlut;  // 1024 cells of [0, 1]
 };
 
-// Exact std::upper_bound count (lloydmax.hpp:46-49) seeded by a 256-cell
-// lookup from an fp32 estimate of x; the fp64 compares that follow make the
-// result exact whatever the seed (normally one compare each way).
+// Exact std::upper_bound count (lloydmax.hpp:46-49) via a 1024-cell bracket
+// table: for the fp32 cell of x, every boundary below lo is < x and every
+// boundary from hi on is > x (the table is built with a 1e-6 guard, far
+// above the fp32 cell-position error), so when hi - lo <= 1 one exact fp64
+// compare decides; wider brackets (> 1 boundary per cell) binary-search.
 __device__ __forceinline__ uint32_t quantize_lut(const double* b, uint32_t nb,
-                                                 const uint8_t* lut, double x, float lo,
+                                                 const uint32_t* lut, double x, float lo,
                                                  float scale) {
   int cell = __float2int_rz(((float)x - lo) * scale);
-  cell = cell < 0 ? 0 : (cell > 255 ? 255 : cell);
-  uint32_t i = lut[cell];
-  i += (i < nb && !(x < b[i])) ? 1u : 0u;
-  i += (i < nb && !(x < b[i])) ? 1u : 0u;
-  i -= (i > 0 && x < b[i - 1]) ? 1u : 0u;
-  const bool ok = (i == nb || x < b[i]) && (i == 0 || !(x < b[i - 1]));
-  return ok ? i : quantize_ub(b, nb, x);  // fallback: > 2 boundaries in reach
+  cell = cell < 0 ? 0 : (cell > 1023 ? 1023 : cell);
+  const uint32_t e = lut[cell], l = e & 0xffff, h = e >> 16;
+  if (h - l <= 1u && x == x) return l + ((l < h && !(x < b[l])) ? 1u : 0u);
+  return quantize_ub(b, nb, x);
 }
 
-// ---- joint rounding of one triplet (codec.hpp:143-195) -------------------
 __device__ __forceinline__ void oct_encode_exact(double t0, double t1, double t2, double& xi,
                                                  double& eta) {
   // octahedral.hpp:22-31
@@ -93,12 +91,12 @@ __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const Co
   double xi, eta;
   oct_encode_exact(t0, t1, t2, xi, eta);
   const uint32_t K = p.K;
-  const uint32_t sx = quantize_lut(s.xb, K - 1, s.xlut, xi, -1.f, 128.f);
-  const uint32_t sy = quantize_lut(s.xb, K - 1, s.xlut, eta, -1.f, 128.f);
+  const uint32_t sx = quantize_lut(s.xb, K - 1, s.xlut, xi, -1.f, 512.f);
+  const uint32_t sy = quantize_lut(s.xb, K - 1, s.xlut, eta, -1.f, 512.f);
   if (p.rounding == 0) {
     double r = dsqrt(dadd(dadd(dmul(t0, t0), dmul(t1, t1)), dmul(t2, t2)));
     r = r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r);
-    const uint32_t ir = quantize_lut(s.rb, p.KR - 1, s.rlut, r, 0.f, 256.f);
+    const uint32_t ir = quantize_lut(s.rb, p.KR - 1, s.rlut, r, 0.f, 1024.f);
     return sx | (sy << 8) | (ir << 16);
   }
   uint32_t ax0 = sx, ax1 = sx, ay0 = sy, ay1 = sy;
@@ -135,12 +133,22 @@ __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const Co
       wb = gt ? b : wb;
     };
     if (p.rounding == 2) {  // fixed 3x3 window, clamped cells predicated off
+      const uint32_t a0 = sx - 1, b0 = sy - 1;  // wrap to huge when sx or sy is 0
+      const bool rv[3] = {a0 < K, true, sx + 1 < K}, cv[3] = {b0 < K, true, sy + 1 < K};
+      const int base = (int)(sx * K + sy);
 #pragma unroll
       for (int da = 0; da < 3; ++da)
 #pragma unroll
         for (int db = 0; db < 3; ++db) {
-          const uint32_t a = sx + da - 1, b = sy + db - 1;  // wraps to huge if < 0
-          cand(a, b, a < K && b < K);
+          const bool valid = rv[da] && cv[db];
+          const float4 nv = valid ? dirs32[base + (da - 1) * (int)K + (db - 1)]
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float sc = valid ? fmaf(f2, nv.z, fmaf(f1, nv.y, f0 * nv.x)) : -INFINITY;
+          const bool gt = sc > b1;
+          b2 = fmaxf(b2, fminf(b1, sc));
+          b1 = fmaxf(b1, sc);
+          wa = gt ? sx + da - 1 : wa;
+          wb = gt ? sy + db - 1 : wb;
         }
     } else {
       for (uint32_t a = ax0; a <= ax1; ++a)
@@ -149,7 +157,7 @@ __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const Co
     if (b1 - b2 > 1e-6f) {  // false for NaN and exact ties
       best = dot3_exact(t0, t1, t2, s.dirs + 3 * (wa * K + wb));
       const double cl = best < 0.0 ? 0.0 : (best > 1.0 ? 1.0 : best);
-      const uint32_t ir = quantize_lut(s.rb, p.KR - 1, s.rlut, cl, 0.f, 256.f);
+      const uint32_t ir = quantize_lut(s.rb, p.KR - 1, s.rlut, cl, 0.f, 1024.f);
       return wa | (wb << 8) | (ir << 16);
     }
   }
@@ -163,7 +171,7 @@ __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const Co
       }
     }
   const double cl = best < 0.0 ? 0.0 : (best > 1.0 ? 1.0 : best);
-  const uint32_t ir = quantize_lut(s.rb, p.KR - 1, s.rlut, cl, 0.f, 256.f);
+  const uint32_t ir = quantize_lut(s.rb, p.KR - 1, s.rlut, cl, 0.f, 1024.f);
   return bx | (by << 8) | (ir << 16);
 }
 
@@ -275,10 +283,10 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
   if (dirs_in_smem) sp += sizeof(double) * 3 * kk;
   float4* d32_s = reinterpret_cast<float4*>(sp);
   if (dirs_in_smem) sp += sizeof(float4) * kk;
-  uint8_t* xlut_s = sp;
-  sp += 256;
-  uint8_t* rlut_s = sp;
-  sp += 256;
+  uint32_t* xlut_s = reinterpret_cast<uint32_t*>(sp);
+  sp += 4096;
+  uint32_t* rlut_s = reinterpret_cast<uint32_t*>(sp);
+  sp += 4096;
   float* gam_s = reinterpret_cast<float*>(sp);
   sp += sizeof(float) * S::VPC;
   uint32_t* sgn_s = reinterpret_cast<uint32_t*>(sp);  // QJL: D/32 words (>=1) per vector
@@ -301,14 +309,9 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
     for (uint32_t i = tid; i < kk; i += blockDim.x)
       d32_s[i] = reinterpret_cast<const float4*>(p.dirs32)[i];
   }
-  for (int c = tid; c < 256; c += blockDim.x) {
-    // number of boundaries strictly below the cell start (a seed, any value works)
-    const double x0 = -1.0 + c / 128.0, r0 = c / 256.0;
-    uint32_t i = 0, j = 0;
-    while (i < p.K - 1 && p.xi_bnd[i] < x0) ++i;
-    while (j < p.KR - 1 && p.rho_bnd[j] < r0) ++j;
-    xlut_s[c] = (uint8_t)i;
-    rlut_s[c] = (uint8_t)j;
+  for (int c = tid; c < 1024; c += blockDim.x) {
+    xlut_s[c] = p.xi_lut[c];
+    rlut_s[c] = p.rho_lut[c];
   }
   __syncthreads();
   const double* dirs64 = dirs_s;
@@ -451,7 +454,7 @@ static size_t compress_smem(const OqCodecParams& p) {
   const uint32_t kk = p.K * p.K;
   size_t b = sizeof(double) * S::VPC * S::STRIDE + 3 * sizeof(double) * 256;
   if (kk <= 1024) b += sizeof(double) * 3 * kk + sizeof(float4) * kk;
-  b += 512;
+  b += 8192;
   b += sizeof(float) * S::VPC + sizeof(uint32_t) * S::VPC * (D >= 32 ? D / 32 : 1) +
        sizeof(uint16_t) * S::VPC + sizeof(uint16_t) * S::VPC * 2 * S::NT + S::VPC * S::NT;
   b = (b + 15) & ~size_t(15);
