@@ -358,8 +358,8 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
       const double t0 = uw[S::pidx(3 * t)], t1 = uw[S::pidx(3 * t + 1)],
                    t2 = uw[S::pidx(3 * t + 2)];
       const uint32_t code = joint_round(p, sm, dirs32, t0, t1, t2);
-      dcode_s[w * 2 * S::NT + 2 * t] = (uint16_t)(code & 0xff);
-      dcode_s[w * 2 * S::NT + 2 * t + 1] = (uint16_t)((code >> 8) & 0xff);
+      // the triplet's 2*b_dir-bit direction field pair, ixi | ieta << b_dir
+      dcode_s[w * 2 * S::NT + t] = (uint16_t)((code & 0xff) | (((code >> 8) & 0xff) << p.b_dir));
       ncode_s[w * S::NT + t] = (uint8_t)(code >> 16);
       if (p.qjl) {
         const uint32_t a = code & 0xff, b = (code >> 8) & 0xff, ir = code >> 16;
@@ -388,49 +388,44 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
     }
     __syncthreads();
 
-    // ---- D: OCTO record assembly (codec.hpp:381-393) ------------------------
-    // Task (key, part): part 0 writes gamma (+ the QJL bytes), part 1 the
-    // direction bit stream, part 2 the norm bit stream; each stream is packed
-    // sequentially through a 64-bit shift register (LSB-first, io.hpp:66-85).
+    // ---- D: OCTO record assembly (codec.hpp:381-393), word-parallel --------
+    // Task (key, k): k = 0 writes gamma (+ the QJL bytes); k in [1, dw] builds
+    // 32-bit word k-1 of the direction stream from the <= 6 triplet field
+    // pairs overlapping it; the rest build the norm stream words.  Streams
+    // are LSB-first with zero padding (io.hpp:66-85).
     const size_t nv = min((size_t)S::VPC, n - blk * S::VPC);
-    for (int task = tid; task < 3 * (int)nv; task += blockDim.x) {
-      const int w = task / 3, part = task - 3 * w;
-      uint8_t* rec = stage_s + w * rb;
-      if (part == 0) {
-        const uint32_t gb = __float_as_uint(gam_s[w]);
+    {
+      const int dw = (p.dir_bytes + 3) >> 2, nw = (p.nrm_bytes + 3) >> 2, per = 1 + dw + nw;
+      const int pb = 2 * p.b_dir, nb = p.b_nrm;
+      for (int task = tid; task < (int)nv * per; task += blockDim.x) {
+        const int w = task / per, k = task - w * per;
+        uint8_t* rec = stage_s + w * rb;
+        if (k == 0) {
+          const uint32_t gb = __float_as_uint(gam_s[w]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) rec[j] = (uint8_t)(gb >> (8 * j));
-        if (p.qjl) {
-          uint8_t* q = rec + 4 + p.dir_bytes + p.nrm_bytes;
-          q[0] = (uint8_t)gr_s[w];
-          q[1] = (uint8_t)(gr_s[w] >> 8);
-          for (int j = 0; j < ((D + 7) >> 3); ++j)
-            q[2 + j] = (uint8_t)(sgn_s[w * SGW + (j >> 2)] >> (8 * (j & 3)));
-        }
-      } else {
-        const bool dir = part == 1;
-        const int bits = dir ? p.b_dir : p.b_nrm, nf = dir ? 2 * S::NT : S::NT;
-        uint8_t* o = rec + (dir ? 4 : 4 + p.dir_bytes);
-        const uint16_t* dc = dcode_s + w * 2 * S::NT;
-        const uint8_t* nc = ncode_s + w * S::NT;
-        uint64_t acc = 0;
-        int nb = 0;
-        auto push = [&](uint32_t code) {
-          acc |= (uint64_t)code << nb;
-          nb += bits;
-          if (nb >= 32) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) o[j] = (uint8_t)(acc >> (8 * j));
-            o += 4;
-            acc >>= 32;
-            nb -= 32;
+          for (int j = 0; j < 4; ++j) rec[j] = (uint8_t)(gb >> (8 * j));
+          if (p.qjl) {
+            uint8_t* q = rec + 4 + p.dir_bytes + p.nrm_bytes;
+            q[0] = (uint8_t)gr_s[w];
+            q[1] = (uint8_t)(gr_s[w] >> 8);
+            for (int j = 0; j < ((D + 7) >> 3); ++j)
+              q[2 + j] = (uint8_t)(sgn_s[w * SGW + (j >> 2)] >> (8 * (j & 3)));
           }
-        };
-        if (dir)
-          for (int f = 0; f < nf; ++f) push(dc[f]);
-        else
-          for (int f = 0; f < nf; ++f) push(nc[f]);
-        for (int j = 0; 8 * j < nb; ++j) o[j] = (uint8_t)(acc >> (8 * j));
+          continue;
+        }
+        const bool dir = k <= dw;
+        const int wi = dir ? k - 1 : k - 1 - dw, bits = dir ? pb : nb;
+        const int b0 = 32 * wi;
+        const int t0 = b0 / bits, t1 = min((b0 + 31) / bits, S::NT - 1);
+        uint32_t word = 0;
+        for (int t = t0; t <= t1; ++t) {
+          const uint32_t c = dir ? (uint32_t)dcode_s[w * 2 * S::NT + t] : (uint32_t)ncode_s[w * S::NT + t];
+          const int sh = t * bits - b0;
+          word |= sh >= 0 ? (c << sh) : (c >> -sh);
+        }
+        const int off = dir ? 4 + 4 * wi : 4 + p.dir_bytes + 4 * wi;
+        const int nbytes = min(4, (dir ? (int)p.dir_bytes : (int)p.nrm_bytes) - 4 * wi);
+        for (int j = 0; j < nbytes; ++j) rec[off + j] = (uint8_t)(word >> (8 * j));
       }
     }
     __syncthreads();
