@@ -32,7 +32,9 @@ struct DecodeShape {
   // different banks when they write their triplets.
   __host__ __device__ static constexpr int pidx(int e) { return LPV > 1 ? e + 4 * (e / EPL) : e; }
   static constexpr int NEED = pidx(3 * NT - 1) + 1;
-  static constexpr int STRIDE = ((NEED + 3) / 4) * 4 + 4;  // float4-aligned rows
+  // float4-aligned rows with STRIDE = 16 (mod 32) floats: the 8 lanes of an
+  // LDS.128 phase (2 keys x 4 lanes) land on 8 distinct 16-byte bank groups
+  static constexpr int STRIDE = ((NEED + 15) / 32) * 32 + 16;
 };
 
 // `bits` (<= 16) at absolute bit position `pos` of a word-aligned smem stream.
@@ -40,6 +42,8 @@ __device__ __forceinline__ uint32_t field(const uint32_t* s, uint32_t pos, uint3
   const uint32_t i = pos >> 5, sh = pos & 31;
   return __funnelshift_r(s[i], s[i + 1], sh) & ((1u << bits) - 1u);
 }
+
+constexpr int kDecRep = 8;  // direction-table replicas (lane & 7)
 
 template <int D, bool TAB>
 __global__ void __launch_bounds__(256) decode_kernel(OqCodecParams p,
@@ -50,7 +54,7 @@ __global__ void __launch_bounds__(256) decode_kernel(OqCodecParams p,
   const uint32_t kk = p.K * p.K;
   uint8_t* sp = smem_raw;
   float4* dirs_s = reinterpret_cast<float4*>(sp);
-  if (TAB) sp += (size_t)kk * 16;
+  if (TAB) sp += (size_t)kk * 16 * kDecRep;
   float* rho_s = reinterpret_cast<float*>(sp);
   sp += 256 * 4;
   float* rows = reinterpret_cast<float*>(sp);
@@ -59,11 +63,15 @@ __global__ void __launch_bounds__(256) decode_kernel(OqCodecParams p,
 
   const int tid = threadIdx.x, lane = tid & 31;
   if (TAB)
-    for (uint32_t i = tid; i < kk; i += blockDim.x)
-      dirs_s[i] = reinterpret_cast<const float4*>(p.dirs32)[i];
+    for (uint32_t i = tid; i < kk * kDecRep; i += blockDim.x)
+      dirs_s[i] = reinterpret_cast<const float4*>(p.dirs32)[i / kDecRep];
   for (uint32_t i = tid; i < p.KR; i += blockDim.x) rho_s[i] = p.rho32[i];
-  const float4* dirs = dirs_s;
-  if constexpr (!TAB) dirs = reinterpret_cast<const float4*>(p.dirs32);
+  const float4* dirs = dirs_s + (lane & (kDecRep - 1));
+  uint32_t dstride = kDecRep;
+  if constexpr (!TAB) {
+    dirs = reinterpret_cast<const float4*>(p.dirs32);
+    dstride = 1;
+  }
 
   const int sub = S::LPV > 1 ? (lane & (S::LPV - 1)) : 0;
   const int vl = tid / S::LPV;
@@ -94,16 +102,46 @@ __global__ void __launch_bounds__(256) decode_kernel(OqCodecParams p,
     if (live) {
       // ---- reconstruct_rotated for this lane's triplets ---------------------
       const uint32_t base = (uint32_t)vl * rb * 8;  // bit position of the record
-      const uint32_t dpos = base + 32, npos = base + 32 + 8 * p.dir_bytes;
+      const uint32_t pb = 2 * p.b_dir, nbits = p.b_nrm;
+      const uint32_t dpos = base + 32 + pb * sub * S::TPL;
+      const uint32_t npos = base + 32 + 8 * p.dir_bytes + nbits * sub * S::TPL;
       g = __uint_as_float(field(stage32, base, 16) | (field(stage32, base + 16, 16) << 16));
-#pragma unroll 4
+      // this lane's TPL field pairs (<= 16 bits each) and norm fields as
+      // word-aligned runs: 2 + TPL/2 and 1 + TPL/4 word loads, one funnel
+      // shift per word, then static-position extraction
+      constexpr int DW = (S::TPL * 16 + 31) / 32, NW = (S::TPL * 8 + 31) / 32;
+      uint32_t dr[DW], nr[NW];
+      {
+        const uint32_t i0 = dpos >> 5, sh = dpos & 31;
+        uint32_t prev = stage32[i0];
+#pragma unroll
+        for (int k = 0; k < DW; ++k) {
+          const uint32_t nxt = stage32[i0 + k + 1];
+          dr[k] = __funnelshift_r(prev, nxt, sh);
+          prev = nxt;
+        }
+        const uint32_t j0 = npos >> 5, sj = npos & 31;
+        prev = stage32[j0];
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+          const uint32_t nxt = stage32[j0 + k + 1];
+          nr[k] = __funnelshift_r(prev, nxt, sj);
+          prev = nxt;
+        }
+      }
+      auto take = [](const uint32_t* w, uint32_t pos, uint32_t bits) {
+        const uint32_t i = pos >> 5, sh = pos & 31;
+        const uint32_t v = sh + bits <= 32 ? (w[i] >> sh) : __funnelshift_r(w[i], w[i + 1], sh);
+        return v & ((1u << bits) - 1u);
+      };
+#pragma unroll
       for (int u = 0; u < S::TPL; ++u) {
         const int t = sub * S::TPL + u;
         if (t < S::NT) {
-          const uint32_t pr = field(stage32, dpos + 2 * p.b_dir * t, 2 * p.b_dir);
+          const uint32_t pr = take(dr, pb * u, pb);
           const uint32_t a = pr & (p.K - 1), b = pr >> p.b_dir;
-          const uint32_t ir = field(stage32, npos + p.b_nrm * t, p.b_nrm);
-          const float4 nv4 = dirs[a * p.K + b];
+          const uint32_t ir = take(nr, nbits * u, nbits);
+          const float4 nv4 = dirs[(a * p.K + b) * dstride];
           const float r = rho_s[ir];
           row[S::pidx(3 * t)] = r * nv4.x;
           if (3 * t + 1 < D) row[S::pidx(3 * t + 1)] = r * nv4.y;
@@ -170,8 +208,8 @@ static cudaError_t launch_decode_dt(const OqCodecParams& p, const uint8_t* recs,
                                     float* out, cudaStream_t st, int num_sms) {
   using S = DecodeShape<D>;
   const uint32_t kk = p.K * p.K;
-  const size_t smem = (TAB ? kk * 16 : 0) + 256 * 4 + (size_t)S::VPC * S::STRIDE * 4 +
-                      (size_t)S::VPC * p.rec_bytes + 32;
+  const size_t smem = (TAB ? kk * 16 * kDecRep : 0) + 256 * 4 +
+                      (size_t)S::VPC * S::STRIDE * 4 + (size_t)S::VPC * p.rec_bytes + 64;
   cudaError_t e = cudaFuncSetAttribute(decode_kernel<D, TAB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -191,7 +229,7 @@ static cudaError_t launch_decode_dt(const OqCodecParams& p, const uint8_t* recs,
 template <int D>
 static cudaError_t launch_decode_d(const OqCodecParams& p, const uint8_t* recs, size_t n,
                                    float* out, cudaStream_t st, int num_sms) {
-  return p.K * p.K <= 4096 ? launch_decode_dt<D, true>(p, recs, n, out, st, num_sms)
+  return p.K * p.K <= 1024 ? launch_decode_dt<D, true>(p, recs, n, out, st, num_sms)
                            : launch_decode_dt<D, false>(p, recs, n, out, st, num_sms);
 }
 
