@@ -150,6 +150,26 @@ oq_status oq_attention_combine(const oq_codec* cv, const float* partials, int ro
                                size_t row_stride, size_t part_stride, int finalize, float* out,
                                void* stream);
 
+/* ---- general path: any codec configuration, straight from OCTO records ----
+ * Encoder::score(prepare(q), k) (codec.hpp:282-316): out[nq][n] fp32 for q
+ * [nq, dim] fp32 against n records. */
+oq_status oq_scores(const oq_codec* codec, const float* q, int nq, const void* records, size_t n,
+                    float* out, void* stream);
+/* attention_decode(enc, q, keys, values, n_splits) (attention.hpp:50-73) with
+ * dense fp32 values [n, vdim] (vdim <= 256), one output row per query:
+ * out [nq, vdim].  n_splits contiguous chunks merged in order. */
+size_t oq_attention_dense_workspace_bytes(int nq, int n_splits, int vdim);
+oq_status oq_attention_decode_dense(const oq_codec* codec, const float* q, int nq,
+                                    const void* records, size_t n, const float* values,
+                                    int vdim, int n_splits, float* out, void* workspace,
+                                    size_t ws_bytes, void* stream);
+
+/* ---- device memory helpers (so C/C++ callers need no CUDA headers) ------- */
+oq_status oq_device_alloc(size_t bytes, void** ptr);
+oq_status oq_device_free(void* ptr);
+oq_status oq_copy_to_device(void* dst, const void* src, size_t bytes);
+oq_status oq_copy_to_host(void* dst, const void* src, size_t bytes);  /* synchronizes */
+
 /* ---- measurement support (bench.py) -------------------------------------
  * When enabled, CUDA events are recorded on the launching stream around each
  * hot kernel ("compress", "decode", "attention"); collect sums them. */

@@ -35,6 +35,7 @@ import numpy as np
 
 __all__ = [
     "CodecConfig", "Encoder", "FormatError", "KVCache", "ROUNDINGS", "attention_decode",
+    "attention_decode_dense",
     "attention_partials", "attention_combine", "default_bit_split",
     "effective_bits_per_coord", "lib", "pack_keys", "parse_rounding", "record_bytes", "rho_book",
     "unpack_keys", "xi_book",
@@ -105,6 +106,9 @@ def lib():
         "oq_attention_partials": ([vp, vp, C.POINTER(_Shape), vp, vp, vp, u64, u64, vp, i32, vp,
                                    sz, vp], i32),
         "oq_attention_combine": ([vp, vp, i32, i32, sz, sz, i32, vp, vp], i32),
+        "oq_scores": ([vp, vp, i32, vp, sz, vp, vp], i32),
+        "oq_attention_dense_workspace_bytes": ([i32, i32, i32], sz),
+        "oq_attention_decode_dense": ([vp, vp, i32, vp, sz, vp, i32, i32, vp, vp, sz, vp], i32),
         "oq_timing_enable": ([i32], None),
         "oq_timing_collect": ([C.c_char_p, C.POINTER(C.c_double), C.POINTER(i32)], i32),
     }
@@ -305,6 +309,17 @@ class Encoder:
         t = torch.from_numpy(k.copy()).cuda().reshape(1, -1)
         return bytes(self.compress(t).cpu().numpy().tobytes())
 
+    def scores(self, q, records, stream=None):
+        """Encoder::score(prepare(q), k) for q [nq, dim] x records [n] -> [nq, n] fp32."""
+        import torch
+        q = q.contiguous().float().reshape(-1, self.cfg.dim)
+        records = records.contiguous()
+        n = records.numel() // self.record_bytes
+        out = torch.empty((q.shape[0], n), dtype=torch.float32, device=q.device)
+        _check(lib().oq_scores(self._h, _ptr(q), q.shape[0], _ptr(records), n, _ptr(out),
+                               _stream(stream)))
+        return out
+
     def tile_bytes(self, role):
         return lib().oq_cache_tile_bytes(self._h, role)
 
@@ -448,6 +463,28 @@ def attention_decode(q, cache: KVCache, n_splits=None, seq_lens=None, T=None, ou
     _check(L.oq_attention_decode(cache.enc_k.handle, cache.enc_v.handle, C.byref(sh), _ptr(q),
                                  _ptr(cache.k), _ptr(cache.v), _ptr(out), n_splits, _ptr(ws),
                                  ws.numel(), _stream(stream)))
+    return out
+
+
+def attention_decode_dense(enc: Encoder, q, records, values, n_splits=1, stream=None):
+    """attention_decode(enc, q, keys, values, n_splits) (attention.hpp:50-73) for any
+    codec config: q [nq, dim] fp32, keys as OCTO records [n], dense values
+    [n, vdim] fp32 -> [nq, vdim]."""
+    import torch
+    q = q.contiguous().float().reshape(-1, enc.cfg.dim)
+    records = records.contiguous()
+    values = values.contiguous().float()
+    n = records.numel() // enc.record_bytes
+    nq, vdim = q.shape[0], values.shape[-1] if values.dim() > 1 else 1
+    if values.shape[0] != n:
+        raise ValueError("values/cache length mismatch")
+    L = lib()
+    ws_bytes = L.oq_attention_dense_workspace_bytes(nq, max(1, n_splits), vdim)
+    ws = _Workspace.get(ws_bytes, q.device)
+    out = torch.empty((nq, vdim), dtype=torch.float32, device=q.device)
+    _check(L.oq_attention_decode_dense(enc.handle, _ptr(q), nq, _ptr(records), n, _ptr(values),
+                                       vdim, n_splits, _ptr(out), _ptr(ws), ws.numel(),
+                                       _stream(stream)))
     return out
 
 

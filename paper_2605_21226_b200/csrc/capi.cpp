@@ -560,6 +560,63 @@ oq_status oq_attention_combine(const oq_codec* cv, const float* partials, int ro
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "combine kernel");
 }
 
+oq_status oq_scores(const oq_codec* c, const float* q, int nq, const void* records, size_t n,
+                    float* out, void* stream) {
+  oq_status s = check_codec(c);
+  if (s) return s;
+  if (nq < 0 || (n && nq && (!q || !records || !out)))
+    return fail(OQ_ERR_INVALID_ARGUMENT, "bad scores arguments");
+  cudaError_t e = oqd::launch_scores(c->p, q, nq, static_cast<const uint8_t*>(records), n, out,
+                                     as_stream(stream), c->num_sms);
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "scores kernel");
+}
+
+size_t oq_attention_dense_workspace_bytes(int nq, int n_splits, int vdim) {
+  if (nq < 1 || n_splits < 1 || vdim < 1) return 0;
+  return oqd::dense_attention_workspace(nq, n_splits, vdim);
+}
+
+oq_status oq_attention_decode_dense(const oq_codec* c, const float* q, int nq,
+                                    const void* records, size_t n, const float* values,
+                                    int vdim, int n_splits, float* out, void* ws,
+                                    size_t ws_bytes, void* stream) {
+  oq_status s = check_codec(c);
+  if (s) return s;
+  // attention.hpp:54-56
+  if (n == 0) return fail(OQ_ERR_INVALID_ARGUMENT, "empty cache");
+  if (n_splits < 1) return fail(OQ_ERR_INVALID_ARGUMENT, "n_splits must be >= 1");
+  if (nq < 1 || !q || !records || !values || !out || !ws)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "null argument");
+  if (vdim < 1 || vdim > 256) return fail(OQ_ERR_UNSUPPORTED, "value width must be in [1, 256]");
+  if (ws_bytes < oq_attention_dense_workspace_bytes(nq, n_splits, vdim))
+    return fail(OQ_ERR_INVALID_ARGUMENT, "workspace too small");
+  cudaError_t e = oqd::launch_dense_attention(c->p, q, nq, static_cast<const uint8_t*>(records), n,
+                                              values, vdim, n_splits, static_cast<float*>(ws),
+                                              out, as_stream(stream));
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "dense attention kernel");
+}
+
+oq_status oq_device_alloc(size_t bytes, void** ptr) {
+  if (!ptr) return fail(OQ_ERR_INVALID_ARGUMENT, "null output pointer");
+  cudaError_t e = cudaMalloc(ptr, bytes ? bytes : 1);
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "cudaMalloc");
+}
+
+oq_status oq_device_free(void* ptr) {
+  cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "cudaFree");
+}
+
+oq_status oq_copy_to_device(void* dst, const void* src, size_t bytes) {
+  cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "cudaMemcpy H2D");
+}
+
+oq_status oq_copy_to_host(void* dst, const void* src, size_t bytes) {
+  cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "cudaMemcpy D2H");
+}
+
 // Kernel timing (bench support): enable/disable, then collect the summed
 // milliseconds and launch count of every timed launch named `name`.
 void oq_timing_enable(int on) {

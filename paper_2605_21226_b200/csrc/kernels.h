@@ -58,4 +58,12 @@ cudaError_t launch_attention_combine(const OqCodecParams& pv, const float* parti
                                      int n_parts, size_t row_stride, size_t part_stride,
                                      int finalize, float* out, cudaStream_t st);
 
+// ---- generic (any codec config) scores / dense-V attention (attention_dense.cu)
+cudaError_t launch_scores(const OqCodecParams& p, const float* q, int nq, const uint8_t* recs,
+                          size_t n, float* out, cudaStream_t st, int num_sms);
+size_t dense_attention_workspace(int nq, int n_splits, int vdim);
+cudaError_t launch_dense_attention(const OqCodecParams& p, const float* q, int nq,
+                                   const uint8_t* recs, size_t n, const float* values, int vdim,
+                                   int n_splits, float* workspace, float* out, cudaStream_t st);
+
 }  // namespace oqd
