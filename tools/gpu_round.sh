@@ -1,7 +1,7 @@
 #!/bin/bash
 # One gpurun call: smoke (+memcheck), GPU parity tests, bench, ncu captures.
 # Stages selectable with STAGES="smoke memcheck pytest bench ncu" (default all).
-cd "$(dirname "$0")"
+cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 STAGES=${STAGES:-"smoke memcheck pytest bench ncu"}
 nvidia-smi > gpurun_out/nvidia-smi.txt 2>&1
