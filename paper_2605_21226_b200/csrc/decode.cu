@@ -12,7 +12,9 @@
 //  3. each lane reloads EPL = D/LPV contiguous coordinates and runs the
 //     inverse rotation in registers — WHT butterflies in-lane, then
 //     log2(LPV) shuffle stages — scales by gamma/sqrt(d), applies the signs
-//     (rotation.hpp:52-56) and stores float4s.
+//     (rotation.hpp:52-56) and writes the row back in place;
+//  4. the CTA streams its contiguous block of VPC output rows to HBM with
+//     coalesced 16-byte streaming stores.
 #include <cstdint>
 
 #include "common.cuh"
@@ -48,7 +50,8 @@ constexpr int kDecRep = 8;  // direction-table replicas (lane & 7)
 template <int D, bool TAB>
 __global__ void __launch_bounds__(256) decode_kernel(OqCodecParams p,
                                                      const uint8_t* __restrict__ recs, size_t n,
-                                                     float* __restrict__ out, int aligned) {
+                                                     float* __restrict__ out, int aligned,
+                                                     int aligned_out) {
   using S = DecodeShape<D>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t kk = p.K * p.K;
@@ -189,15 +192,26 @@ __global__ void __launch_bounds__(256) decode_kernel(OqCodecParams p,
       const float v = y[i] * gs;
       y[i] = ((smask >> i) & 1u) ? -v : v;
     }
-    if (live) {
-      float* o = out + (v0 + vl) * D + e0;
-      if constexpr (S::EPL % 4 == 0) {
+    // ---- stage the decoded row in place, then stream the block out --------
+    // (a lane's 32 contiguous floats would make every warp store touch 32
+    // different 512-byte keys; the block's keys are one contiguous range, so
+    // the CTA writes it with fully coalesced 16-byte streaming stores)
 #pragma unroll
-        for (int i = 0; i < S::EPL; i += 4)
-          *reinterpret_cast<float4*>(o + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < S::EPL; ++i) o[i] = y[i];
+    for (int i = 0; i < S::EPL; i += 4)
+      *reinterpret_cast<float4*>(row + S::pidx(e0 + i)) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
+    __syncthreads();
+    float* o = out + v0 * D;
+    const int nf4 = (int)nv * (D / 4);
+    if (aligned_out) {
+      for (int f = tid; f < nf4; f += blockDim.x) {
+        const int k = f / (D / 4), e = 4 * (f % (D / 4));
+        __stcs(reinterpret_cast<float4*>(o) + f,
+               *reinterpret_cast<const float4*>(rows + k * S::STRIDE + S::pidx(e)));
+      }
+    } else {
+      for (int f = tid; f < nf4 * 4; f += blockDim.x) {
+        const int k = f / D, e = f % D;
+        o[f] = rows[k * S::STRIDE + S::pidx(e)];
       }
     }
   }
@@ -222,7 +236,9 @@ static cudaError_t launch_decode_dt(const OqCodecParams& p, const uint8_t* recs,
   size_t grid = (size_t)per_sm * num_sms;
   if (grid > nblk) grid = nblk;
   const int aligned = (reinterpret_cast<uintptr_t>(recs) & 15) == 0;
-  decode_kernel<D, TAB><<<(unsigned)grid, S::THREADS, smem, st>>>(p, recs, n, out, aligned);
+  const int aligned_out = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  decode_kernel<D, TAB><<<(unsigned)grid, S::THREADS, smem, st>>>(p, recs, n, out, aligned,
+                                                                  aligned_out);
   return cudaGetLastError();
 }
 
