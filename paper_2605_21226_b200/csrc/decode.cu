@@ -2,7 +2,11 @@
 // fp32 on sm_100a.  HBM-bound target: reads rec_bytes and writes 4*D bytes
 // per key.
 //
-// A CTA of 256 threads decodes VPC keys per iteration:
+// Two kernels: decode128_kernel<b_dir, b_nrm> (d = 128 at the BASELINE bit
+// splits (3,1), (4,2), (5,3): one key per thread, records double-buffered by
+// TMA, see below) and the generic decode_kernel<D> for every other config.
+//
+// Generic: a CTA of 256 threads decodes VPC keys per iteration:
 //  1. the block of records is staged in shared memory with 16-byte loads;
 //  2. LPV = max(1, D/32) lanes per key each take a run of triplets, pull the
 //     direction pair and norm index out of the record with two aligned word
@@ -16,6 +20,7 @@
 //  4. the CTA streams its contiguous block of VPC output rows to HBM with
 //     coalesced 16-byte streaming stores.
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -217,6 +222,215 @@ __global__ void __launch_bounds__(256) decode_kernel(OqCodecParams p,
   }
 }
 
+// ---------------------------------------------------------------------------
+// d = 128 fast path: ONE KEY PER THREAD.  The record's fields sit at
+// compile-time bit positions (b_dir, b_nrm template parameters), so every
+// triplet is extracted with static shifts straight into the thread's 128
+// registers; the whole inverse WHT (7 butterfly stages) runs in registers
+// with no shuffles, signs and gamma/sqrt(d) are folded into one multiply per
+// coordinate, and each warp transposes its 32 decoded keys through shared
+// memory (two 64-coordinate halves) so that global stores are 256-byte
+// segments.  Shared traffic per key: record staging, 43 direction + 43 norm
+// lookups and the output transpose.
+constexpr int kD128Threads = 128;            // 4 warps, 128 keys per block
+constexpr int kD128Rep = 8;                  // direction-table replicas (lane & 7)
+constexpr int kD128HalfStride = 68;          // floats per staged half row (64 + 4)
+
+template <int BD, int BN>
+struct D128 {
+  static constexpr int NT = 43;
+  static constexpr int DIRB = (2 * NT * BD + 7) / 8, NRMB = (NT * BN + 7) / 8;
+  static constexpr int BYTES = 4 + DIRB + NRMB;           // without the QJL sidecar
+  static constexpr int WORDS = (BYTES + 3) / 4;           // aligned record words used
+  static constexpr int NPAIR = 1 << (2 * BD), NRHO = 1 << BN;
+};
+
+// `bits` (<= 16) at static bit position `pos` of the thread's record words.
+template <int N>
+__device__ __forceinline__ uint32_t recfield(const uint32_t (&w)[N], int pos, int bits) {
+  const int i = pos >> 5, sh = pos & 31;
+  const uint32_t v = (sh + bits <= 32) ? (w[i] >> sh) : __funnelshift_r(w[i], w[i + 1], sh);
+  return v & ((1u << bits) - 1u);
+}
+
+// 1-D TMA (cp.async.bulk) into shared memory completing on an mbarrier.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int BD, int BN>
+__global__ void __launch_bounds__(kD128Threads, 3) decode128_kernel(OqCodecParams p,
+                                                                 const uint8_t* __restrict__ recs,
+                                                                 size_t n, float* __restrict__ out,
+                                                                 int aligned) {
+  using S = D128<BD, BN>;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  float4* dirs_s = reinterpret_cast<float4*>(smem_raw);                // [NPAIR][kD128Rep]
+  float* rho_s = reinterpret_cast<float*>(dirs_s + S::NPAIR * kD128Rep);  // [NRHO]
+  float* half_s = rho_s + 16;                                           // [4 warps][32][68]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(half_s + 4 * 32 * kD128HalfStride);  // [2]
+  uint8_t* stage0 = reinterpret_cast<uint8_t*>(bars + 2);  // 2 x [128 records], 16-aligned
+  const uint32_t rb = p.rec_bytes;
+  const uint32_t stage_bytes = (kD128Threads * rb + 15) & ~15u;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // direction table in field-pair order pr = ixi | ieta << b_dir
+  for (int i = tid; i < S::NPAIR * kD128Rep; i += kD128Threads) {
+    const int pr = i / kD128Rep, a = pr & ((1 << BD) - 1), b = pr >> BD;
+    dirs_s[i] = reinterpret_cast<const float4*>(p.dirs32)[(a << BD) | b];
+  }
+  for (int i = tid; i < S::NRHO; i += kD128Threads) rho_s[i] = p.rho32[i];
+  const float4* dtab = dirs_s + (lane & (kD128Rep - 1));
+  float* hs = half_s + warp * 32 * kD128HalfStride;
+  const float isd = (float)p.inv_sqrt_d;
+  const size_t nblk = (n + kD128Threads - 1) / kD128Threads;
+  // Records of full blocks arrive by TMA, double-buffered one block ahead;
+  // the (single) partial tail block is copied by the threads.
+  auto full_block = [&](size_t b) { return aligned && (b + 1) * kD128Threads <= n; };
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (blockIdx.x < nblk && full_block(blockIdx.x))
+      bulk_g2s(stage0, recs + (size_t)blockIdx.x * kD128Threads * rb, kD128Threads * rb, &bars[0]);
+  }
+
+  uint32_t it = 0;
+  for (size_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
+    const size_t v0 = blk * kD128Threads;
+    const int nv = (int)min((size_t)kD128Threads, n - v0);
+    uint8_t* stage = stage0 + (it & 1) * stage_bytes;
+    __syncthreads();  // every thread is done with the other buffer (and the tables are in)
+    if (tid == 0) {
+      const size_t nb = blk + gridDim.x;
+      if (nb < nblk && full_block(nb)) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bulk_g2s(stage0 + ((it + 1) & 1) * stage_bytes, recs + nb * kD128Threads * rb,
+                 kD128Threads * rb, &bars[(it + 1) & 1]);
+      }
+    }
+    if (full_block(blk)) {
+      mbar_wait(&bars[it & 1], (it >> 1) & 1);
+    } else {
+      const size_t nbytes = (size_t)nv * rb;
+      const uint8_t* src = recs + v0 * rb;
+      for (size_t i = tid; i < nbytes; i += kD128Threads) stage[i] = src[i];
+      __syncthreads();
+    }
+
+    // ---- this thread's record -> 128 rotated-frame coordinates ---------------
+    float y[128];
+    float gs = 0.f;
+    {
+      uint32_t w[S::WORDS + 1];
+      const uint32_t off = (uint32_t)tid * rb, wi = off >> 2, sh = 8 * (off & 3);
+      const uint32_t* st32 = reinterpret_cast<const uint32_t*>(stage);
+      uint32_t prev = st32[wi];
+#pragma unroll
+      for (int k = 0; k < S::WORDS; ++k) {
+        const uint32_t nxt = st32[wi + k + 1];
+        w[k] = __funnelshift_r(prev, nxt, sh);
+        prev = nxt;
+      }
+      w[S::WORDS] = 0u;
+      gs = __uint_as_float(w[0]) * isd;  // codec.hpp:273 (x float gamma), rotation.hpp:29
+#pragma unroll
+      for (int t = 0; t < S::NT; ++t) {
+        const uint32_t pr = recfield(w, 32 + 2 * BD * t, 2 * BD);
+        const uint32_t ir = recfield(w, 32 + 8 * S::DIRB + BN * t, BN);
+        const float4 d4 = dtab[pr * kD128Rep];
+        const float r = rho_s[ir];
+        y[3 * t] = r * d4.x;  // reconstruct_rotated, codec.hpp:252-266
+        if (3 * t + 1 < 128) y[3 * t + 1] = r * d4.y;
+        if (3 * t + 2 < 128) y[3 * t + 2] = r * d4.z;
+      }
+    }
+    // ---- inverse rotation: H y, then signs and gamma/sqrt(d) -----------------
+#pragma unroll
+    for (int len = 1; len < 128; len <<= 1)
+#pragma unroll
+      for (int i = 0; i < 128; ++i)
+        if (!(i & len)) {
+          const float a = y[i], b = y[i + len];
+          y[i] = a + b;
+          y[i + len] = a - b;
+        }
+#pragma unroll
+    for (int i = 0; i < 128; ++i) {
+      const bool neg = (p.sign_mask[i >> 5] >> (i & 31)) & 1u;  // uniform
+      y[i] *= neg ? -gs : gs;
+    }
+    // ---- per-warp transpose through shared memory, two halves ----------------
+    const int kw0 = warp * 32;  // this warp's first key in the block
+    const int nkw = min(32, nv - kw0);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        *reinterpret_cast<float4*>(hs + lane * kD128HalfStride + 4 * i) =
+            make_float4(y[64 * h + 4 * i], y[64 * h + 4 * i + 1], y[64 * h + 4 * i + 2],
+                        y[64 * h + 4 * i + 3]);
+      __syncwarp();
+      // 32 keys x 16 float4 of this half: lane -> (key = it*2 + lane/16, f4 = lane%16)
+      if (nkw > 0) {
+        float* ob = out + (v0 + kw0) * 128 + 64 * h;
+#pragma unroll 4
+        for (int it = 0; it < 16; ++it) {
+          const int k = 2 * it + (lane >> 4), f = lane & 15;
+          if (k < nkw) {
+            const float4 v = *reinterpret_cast<const float4*>(hs + k * kD128HalfStride + 4 * f);
+            __stcs(reinterpret_cast<float4*>(ob + (size_t)k * 128) + f, v);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <int BD, int BN>
+static cudaError_t launch_decode128(const OqCodecParams& p, const uint8_t* recs, size_t n,
+                                   float* out, cudaStream_t st, int num_sms) {
+  using S = D128<BD, BN>;
+  const size_t smem = (size_t)S::NPAIR * kD128Rep * 16 + 16 * 4 + 4 * 32 * kD128HalfStride * 4 +
+                      16 + 2 * (((size_t)kD128Threads * p.rec_bytes + 15) & ~size_t(15)) + 64;
+  cudaError_t e = cudaFuncSetAttribute(decode128_kernel<BD, BN>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode128_kernel<BD, BN>,
+                                                    kD128Threads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const size_t nblk = (n + kD128Threads - 1) / kD128Threads;
+  size_t grid = (size_t)per_sm * num_sms;
+  if (grid > nblk) grid = nblk;
+  const int aligned = (reinterpret_cast<uintptr_t>(recs) & 15) == 0;
+  decode128_kernel<BD, BN><<<(unsigned)grid, kD128Threads, smem, st>>>(p, recs, n, out, aligned);
+  return cudaGetLastError();
+}
+
 template <int D, bool TAB>
 static cudaError_t launch_decode_dt(const OqCodecParams& p, const uint8_t* recs, size_t n,
                                     float* out, cudaStream_t st, int num_sms) {
@@ -252,6 +466,11 @@ static cudaError_t launch_decode_d(const OqCodecParams& p, const uint8_t* recs, 
 cudaError_t launch_decode(const OqCodecParams& p, const uint8_t* recs, size_t n, float* out,
                           cudaStream_t st, int num_sms) {
   if (n == 0) return cudaSuccess;
+  if (p.dim == 128 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 && !getenv("OQ_DECODE_GENERIC")) {
+    if (p.b_dir == 3 && p.b_nrm == 1) return launch_decode128<3, 1>(p, recs, n, out, st, num_sms);
+    if (p.b_dir == 4 && p.b_nrm == 2) return launch_decode128<4, 2>(p, recs, n, out, st, num_sms);
+    if (p.b_dir == 5 && p.b_nrm == 3) return launch_decode128<5, 3>(p, recs, n, out, st, num_sms);
+  }
   switch (p.dim) {
     case 4: return launch_decode_d<4>(p, recs, n, out, st, num_sms);
     case 8: return launch_decode_d<8>(p, recs, n, out, st, num_sms);
