@@ -87,6 +87,12 @@ oq_status oq_codec_config(const oq_codec* codec, oq_config* cfg);
  * fp64 reference. */
 oq_status oq_compress(const oq_codec* codec, const void* x, int dtype, size_t n, void* records,
                       void* stream);
+/* As oq_compress, and *flagged (device uint32, may be NULL) receives how many
+ * keys the certified fp32 pass could not decide and re-encoded on the exact
+ * fp64 path (0 when the exact kernel ran for every key).  Replaces the same
+ * reference entry point as oq_compress (codec.hpp:214-249). */
+oq_status oq_compress_ex(const oq_codec* codec, const void* x, int dtype, size_t n,
+                         void* records, uint32_t* flagged, void* stream);
 
 /* ---- decode: Encoder::decode (codec.hpp:268-275) -------------------------
  * records -> out device [n, dim] fp32. */

@@ -93,6 +93,7 @@ def lib():
         "oq_codec_create_custom": ([cfgp, dp, i32, dp, i32, C.POINTER(vp)], i32),
         "oq_codec_destroy": ([vp], None),
         "oq_compress": ([vp, vp, i32, sz, vp, vp], i32),
+        "oq_compress_ex": ([vp, vp, i32, sz, vp, vp, vp], i32),
         "oq_decode": ([vp, vp, sz, vp, vp], i32),
         "oq_wire_header": ([cfgp, u64, C.c_char_p], i32),
         "oq_wire_parse_header": ([C.c_char_p, sz, cfgp, C.POINTER(u64)], i32),
@@ -262,8 +263,11 @@ class Encoder:
     def config(self):
         return self.cfg
 
-    def compress(self, x, out=None, stream=None):
-        """Encoder::encode over rows of a CUDA tensor -> uint8 [n, record_bytes]."""
+    def compress(self, x, out=None, stream=None, flagged=None):
+        """Encoder::encode over rows of a CUDA tensor -> uint8 [n, record_bytes].
+
+        flagged: optional CUDA int32 tensor of one element that receives how
+        many keys the certified fp32 pass sent to the exact fp64 path."""
         import torch
         if not x.is_cuda:
             raise ValueError("compress expects a CUDA tensor (there is no CPU path)")
@@ -276,7 +280,8 @@ class Encoder:
             raise ValueError(f"unsupported dtype {x.dtype}")
         if out is None:
             out = torch.empty((n, self.record_bytes), dtype=torch.uint8, device=x.device)
-        _check(lib().oq_compress(self._h, _ptr(x), dt, n, _ptr(out), _stream(stream)))
+        fl = None if flagged is None else _ptr(flagged)
+        _check(lib().oq_compress_ex(self._h, _ptr(x), dt, n, _ptr(out), fl, _stream(stream)))
         return out
 
     def decode(self, records, out=None, stream=None):

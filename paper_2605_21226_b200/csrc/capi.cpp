@@ -326,6 +326,11 @@ oq_status oq_codec_config(const oq_codec* c, oq_config* cfg) {
 
 oq_status oq_compress(const oq_codec* c, const void* x, int dtype, size_t n, void* records,
                       void* stream) {
+  return oq_compress_ex(c, x, dtype, n, records, nullptr, stream);
+}
+
+oq_status oq_compress_ex(const oq_codec* c, const void* x, int dtype, size_t n, void* records,
+                         uint32_t* flagged, void* stream) {
   oq_status s = check_codec(c);
   if (s) return s;
   if (n && (!x || !records)) return fail(OQ_ERR_INVALID_ARGUMENT, "null buffer");
@@ -333,7 +338,7 @@ oq_status oq_compress(const oq_codec* c, const void* x, int dtype, size_t n, voi
     return fail(OQ_ERR_INVALID_ARGUMENT, "unknown dtype");
   TimedScope ts("compress", as_stream(stream));
   cudaError_t e = oqd::launch_compress(c->p, x, dtype, n, static_cast<uint8_t*>(records),
-                                       as_stream(stream), c->num_sms);
+                                       as_stream(stream), c->num_sms, flagged);
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "compress kernel");
 }
 

@@ -21,6 +21,7 @@
 // (SURVEY.md §7 H1).  The grid is persistent, so codebook tables are staged
 // into shared memory once per CTA.
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -257,10 +258,14 @@ __device__ __forceinline__ double seq_sumsq(const double (&x)[CompressShape<D>::
 
 // TAB: codebook tables staged in shared memory (K^2 <= 1024, i.e. b_dir <= 5);
 // otherwise they are read from global memory (L1-cached).
+// list != nullptr: encode only the keys list[0 .. *list_n) (the fast path's
+// flagged keys), each record written at its own key's slot.
 template <int D, bool TAB>
 __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const void* __restrict__ x,
                                                        int dtype, size_t n,
-                                                       uint8_t* __restrict__ out, int aligned) {
+                                                       uint8_t* __restrict__ out, int aligned,
+                                                       const uint32_t* __restrict__ list,
+                                                       const uint32_t* __restrict__ list_n) {
   using S = CompressShape<D>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -324,17 +329,19 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
 
   const uint32_t smask = p.sign_mask[(sub * S::EPL) >> 5] >> ((sub * S::EPL) & 31);
   const uint32_t qmask = p.qsign_mask[(sub * S::EPL) >> 5] >> ((sub * S::EPL) & 31);
+  if (list) n = *list_n;
   const size_t nblocks = (n + S::VPC - 1) / S::VPC;
   const uint32_t rb = p.rec_bytes;
 
   for (size_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
     const size_t v = blk * S::VPC + vl;
     const bool live = v < n;
+    const size_t key = list ? (live ? (size_t)list[v] : 0) : v;
     double* ur = ur_s + vl * S::STRIDE;
 
     // ---- load, norm, normalize (codec.hpp:219-225) ------------------------
     double xv[S::EPL];
-    load_row<S::EPL>(xv, x, dtype, v * D + sub * S::EPL, live);
+    load_row<S::EPL>(xv, x, dtype, key * D + sub * S::EPL, live);
     const double g2 = seq_sumsq<D>(xv, sub, lane);
     const double gamma = dsqrt(g2);
     const double inv = ddiv(1.0, gamma > 1e-12 ? gamma : 1e-12);
@@ -431,7 +438,12 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
     __syncthreads();
     const size_t nbytes = nv * rb;
     uint8_t* dst = out + blk * S::VPC * (size_t)rb;
-    if (aligned) {
+    if (list) {
+      for (size_t i = tid; i < nbytes; i += blockDim.x) {
+        const size_t w = i / rb;
+        out[(size_t)list[blk * S::VPC + w] * rb + (i - w * rb)] = stage_s[i];
+      }
+    } else if (aligned) {
       const uint32_t* src32 = reinterpret_cast<const uint32_t*>(stage_s);
       uint32_t* dst32 = reinterpret_cast<uint32_t*>(dst);
       for (size_t i = tid; i < nbytes / 4; i += blockDim.x) dst32[i] = src32[i];
@@ -459,7 +471,8 @@ static size_t compress_smem(const OqCodecParams& p) {
 
 template <int D, bool TAB>
 static cudaError_t launch_compress_dt(const OqCodecParams& p, const void* x, int dtype, size_t n,
-                                     uint8_t* out, cudaStream_t st, int num_sms) {
+                                     uint8_t* out, cudaStream_t st, int num_sms,
+                                     const uint32_t* list, const uint32_t* list_n) {
   using S = CompressShape<D>;
   const size_t smem = compress_smem<D>(p);
   cudaError_t e = cudaFuncSetAttribute(compress_kernel<D, TAB>,
@@ -469,24 +482,47 @@ static cudaError_t launch_compress_dt(const OqCodecParams& p, const void* x, int
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compress_kernel<D, TAB>, S::THREADS, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  const size_t nblocks = (n + S::VPC - 1) / S::VPC;
+  const size_t nblocks = (n + S::VPC - 1) / S::VPC;  // list mode: n = capacity
   size_t grid = (size_t)per_sm * num_sms;
   if (grid > nblocks) grid = nblocks;
   const int aligned = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
-  compress_kernel<D, TAB><<<(unsigned)grid, S::THREADS, smem, st>>>(p, x, dtype, n, out, aligned);
+  compress_kernel<D, TAB><<<(unsigned)grid, S::THREADS, smem, st>>>(p, x, dtype, n, out, aligned,
+                                                                    list, list_n);
   return cudaGetLastError();
 }
 
 template <int D>
 static cudaError_t launch_compress_d(const OqCodecParams& p, const void* x, int dtype, size_t n,
-                                     uint8_t* out, cudaStream_t st, int num_sms) {
-  return p.K * p.K <= 1024 ? launch_compress_dt<D, true>(p, x, dtype, n, out, st, num_sms)
-                           : launch_compress_dt<D, false>(p, x, dtype, n, out, st, num_sms);
+                                     uint8_t* out, cudaStream_t st, int num_sms,
+                                     const uint32_t* list = nullptr,
+                                     const uint32_t* list_n = nullptr) {
+  return p.K * p.K <= 1024
+             ? launch_compress_dt<D, true>(p, x, dtype, n, out, st, num_sms, list, list_n)
+             : launch_compress_dt<D, false>(p, x, dtype, n, out, st, num_sms, list, list_n);
 }
 
 cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, size_t n,
-                            uint8_t* out, cudaStream_t st, int num_sms) {
+                            uint8_t* out, cudaStream_t st, int num_sms, uint32_t* flagged) {
   if (n == 0) return cudaSuccess;
+  if (compress_fast_ok(p, dtype, x, out) && !getenv("OQ_COMPRESS_EXACT")) {
+    // certified fp32 pass, then the exact kernel over the keys it flagged
+    uint32_t* ws = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), (n + 4) * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(ws, 0, sizeof(uint32_t), st);
+    if (e == cudaSuccess)
+      e = launch_compress_fast(p, static_cast<const float*>(x), n, out, ws + 4, ws, st, num_sms);
+    if (e == cudaSuccess)
+      e = launch_compress_d<128>(p, x, dtype, n, out, st, num_sms, ws + 4, ws);
+    if (e == cudaSuccess && flagged)
+      e = cudaMemcpyAsync(flagged, ws, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
+    const cudaError_t f = cudaFreeAsync(ws, st);
+    return e != cudaSuccess ? e : f;
+  }
+  if (flagged) {
+    cudaError_t e = cudaMemsetAsync(flagged, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+  }
   switch (p.dim) {
     case 4: return launch_compress_d<4>(p, x, dtype, n, out, st, num_sms);
     case 8: return launch_compress_d<8>(p, x, dtype, n, out, st, num_sms);

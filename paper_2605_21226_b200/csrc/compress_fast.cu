@@ -1,0 +1,414 @@
+// compress_fast.cu — K1 fast path: Encoder::encode (codec.hpp:214-249) for
+// d = 128, fp32 keys, scalar / local3x3 rounding, no QJL, at the BASELINE bit
+// splits (3,1), (4,2), (5,3).  ONE KEY PER THREAD, certified fp32:
+//
+//  * each warp owns 32 consecutive keys; every lane pulls its 512-byte row
+//    into a padded shared-memory row with a 1-D TMA bulk copy (mbarrier per
+//    warp), the next block's rows are requested as soon as the current ones
+//    sit in registers;
+//  * gamma is the reference's sequential fp64 sum of squares, replayed
+//    exactly (the fp32 squares are exact in fp64, so fma(k, k, s) == s + k*k)
+//    and stored as float(gamma) (codec.hpp:219-233);
+//  * the rotation runs in fp32 registers (signs, 7-stage WHT, one scale by
+//    float(inv / sqrt(d))).  Its error against the reference's fp64 rotated
+//    coordinates is bounded: |ur32 - ur64| <= E0 = 9.1 u (u = 2^-24; 7 u
+//    ||k||_1 / (gamma sqrt d) <= 7 u from the butterflies, 2 u from the
+//    scale, |ur| <= 1), see DESIGN.md §2;
+//  * every decision of the triplet encoder — octahedral hemisphere and
+//    signs (octahedral.hpp:22-31), the xi/eta bucket (lloydmax.hpp:46-49),
+//    the 3x3 argmax (codec.hpp:164-189) and the norm bucket — is taken in
+//    fp32 and CERTIFIED: it must clear its decision boundary by more than the
+//    propagated error bound, otherwise the key is flagged;
+//  * flagged keys are appended to a list and re-encoded afterwards by the
+//    exact fp64 kernel (compress.cu), so every record is bit-identical to the
+//    reference; the flagged count is reported.
+//  * records are assembled in registers at compile-time bit positions,
+//    merged across lanes at shared word boundaries with one shuffle, and the
+//    warp's 32 records leave with one TMA bulk store.
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace oqd {
+
+constexpr int kCFWarps = 8;
+constexpr int kCFThreads = 32 * kCFWarps;
+constexpr int kCFRow = 132;  // floats per staged row (128 + 4 pad: conflict-free LDS.128)
+constexpr int kCFCells = 128, kCFLutRep = 8;  // LUT: float4 entries, 8 replicas
+
+template <int BD, int BN>
+struct CFS {
+  static constexpr int K = 1 << BD, KR = 1 << BN, NT = 43;
+  static constexpr int DIRB = (2 * NT * BD + 7) / 8, NRMB = (NT * BN + 7) / 8;
+  static constexpr int RB = 4 + DIRB + NRMB;  // record bytes (no QJL)
+  static constexpr int RW = (RB + 3) / 4;     // record words
+  static constexpr int DREP = BD <= 4 ? 8 : 2;
+  static constexpr int RECBUF_WORDS = (32 * RB) / 4 + 4;
+  // shared memory carve (bytes)
+  static constexpr int KP = K + 2;  // direction grid padded by a -inf border
+  static constexpr int DIRS_BYTES = KP * KP * DREP * 16;
+  static constexpr int LUT_BYTES = kCFCells * kCFLutRep * 16;
+  static constexpr int BND_BYTES = 64 * 4;
+  static constexpr int ROWS_BYTES = kCFWarps * 32 * kCFRow * 4;
+  static constexpr int RECB_BYTES = kCFWarps * RECBUF_WORDS * 4;
+  static constexpr int SCR_BYTES = kCFWarps * 32 * (RW + 1) * 4;  // per-lane record words
+  static constexpr int SMEM =
+      DIRS_BYTES + LUT_BYTES + BND_BYTES + ROWS_BYTES + RECB_BYTES + SCR_BYTES + 64;
+};
+
+__device__ __forceinline__ uint32_t cf_smem(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Bucket of x among the xi boundaries = std::upper_bound count
+// (lloydmax.hpp:46-49), certified when x clears both bracketing boundaries by
+// more than g.  One LDS.128 per lookup: cell c of [-1, 1] holds
+// (lo, b[lo], b[lo+1], b[lo+2]) with b[0] = -inf, b[K] = b[K+1] = +inf and lo =
+// the number of boundaries below the cell; a cell holding two or more
+// boundaries stores lo = -1 and flags.
+__device__ __forceinline__ uint32_t cf_bucket(float x, float g, const float4* lut, bool& ok) {
+  int cell = __float2int_rd((x + 1.f) * (0.5f * kCFCells));
+  cell = cell < 0 ? 0 : (cell > kCFCells - 1 ? kCFCells - 1 : cell);
+  const float4 e = lut[cell * kCFLutRep];
+  const int lo = __float_as_int(e.x);
+  const bool upx = x >= e.z;
+  const float bl = upx ? e.z : e.y, bh = upx ? e.w : e.z;
+  ok = ok && lo >= 0 && (x - bl > g) && (bh - x > g);
+  return (uint32_t)lo + (upx ? 1u : 0u);
+}
+
+template <int BD, int BN, int MODE>
+__global__ void __launch_bounds__(kCFThreads, 1)
+    compress_fast_kernel(OqCodecParams p, const float* __restrict__ x, size_t n,
+                         uint8_t* __restrict__ out, uint32_t* __restrict__ flag_idx,
+                         uint32_t* __restrict__ flag_cnt) {
+  using S = CFS<BD, BN>;
+  constexpr int K = S::K;
+  constexpr float U = 5.9604645e-8f;  // 2^-24
+  constexpr float E0 = 9.1f * U;      // |ur32 - ur64| bound (see the header)
+  extern __shared__ __align__(128) uint8_t smem[];
+  float4* dirs = reinterpret_cast<float4*>(smem);
+  float4* lut = reinterpret_cast<float4*>(smem + S::DIRS_BYTES);
+  float* bnd = reinterpret_cast<float*>(smem + S::DIRS_BYTES + S::LUT_BYTES);
+  float* rows = reinterpret_cast<float*>(smem + S::DIRS_BYTES + S::LUT_BYTES + S::BND_BYTES);
+  uint32_t* recb = reinterpret_cast<uint32_t*>(smem + S::DIRS_BYTES + S::LUT_BYTES +
+                                               S::BND_BYTES + S::ROWS_BYTES);
+  uint32_t* scratch_all = recb + kCFWarps * S::RECBUF_WORDS;
+  __shared__ __align__(8) uint64_t bars[kCFWarps];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // ---- tables -------------------------------------------------------------
+  // cell (a + 1, b + 1) = (n_hat(a, b), bias 0); border cells (0, 0, 0, -inf)
+  // so every 3x3 window is 9 loads at immediate offsets and out-of-range
+  // candidates score -inf (codec.hpp:164-176 clamps the window)
+  for (int i = tid; i < S::KP * S::KP * S::DREP; i += kCFThreads) {
+    const int cell = i / S::DREP, a = cell / S::KP - 1, b = cell % S::KP - 1;
+    float4 v = make_float4(0.f, 0.f, 0.f, -INFINITY);
+    if (a >= 0 && a < K && b >= 0 && b < K) {
+      v = reinterpret_cast<const float4*>(p.dirs32)[a * K + b];
+      v.w = 0.f;
+    }
+    dirs[i] = v;
+  }
+  if (tid <= K) bnd[tid] = tid == 0 ? -INFINITY : (tid == K ? INFINITY : (float)p.xi_bnd[tid - 1]);
+  __syncthreads();
+  for (int c = tid; c < kCFCells; c += kCFThreads) {
+    // guard band 1e-6 >> the fp32 error of the cell index
+    const float x0 = -1.f + (float)c / (0.5f * kCFCells) - 1e-6f;
+    const float x1 = -1.f + (float)(c + 1) / (0.5f * kCFCells) + 1e-6f;
+    int l = 0, h = 0;
+    for (int i = 1; i < K; ++i) {
+      l += bnd[i] < x0 ? 1 : 0;
+      h += bnd[i] <= x1 ? 1 : 0;
+    }
+    auto bb = [&](int i) { return i >= K ? INFINITY : bnd[i]; };
+    const float4 v = make_float4(__int_as_float(h - l <= 1 ? l : -1), bb(l), bb(l + 1), bb(l + 2));
+    for (int r = 0; r < kCFLutRep; ++r) lut[c * kCFLutRep + r] = v;
+  }
+  float rbnd[S::KR - 1];
+#pragma unroll
+  for (int i = 0; i < S::KR - 1; ++i) rbnd[i] = (float)p.rho_bnd[i];
+  const float4* dtab = dirs + (lane & (S::DREP - 1));
+  const float4* mylut = lut + (lane & (kCFLutRep - 1));
+  float* myrow = rows + (warp * 32 + lane) * kCFRow;
+  uint32_t* wrec = recb + warp * S::RECBUF_WORDS;
+  uint32_t* scratch = scratch_all + warp * 32 * (S::RW + 1);
+  uint64_t* bar = &bars[warp];
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cf_smem(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const size_t nblk = (n + 31) / 32;
+  const size_t wstride = (size_t)gridDim.x * kCFWarps;
+  auto request = [&](size_t blk) {  // rows of block blk -> this warp's staging rows
+    const size_t k0 = blk * 32;
+    const int nk = (int)min((size_t)32, n - k0);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cf_smem(bar)),
+                   "r"(nk * 512)
+                   : "memory");
+    __syncwarp();
+    if (lane < nk)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, "
+          "[%2];" ::"r"(cf_smem(myrow)),
+          "l"(x + (k0 + lane) * 128), "r"(cf_smem(bar))
+          : "memory");
+  };
+  size_t blk = (size_t)blockIdx.x * kCFWarps + warp;
+  if (blk < nblk) request(blk);
+  uint32_t phase = 0;
+  for (; blk < nblk; blk += wstride, phase ^= 1) {
+    const size_t k0 = blk * 32;
+    const int nk = (int)min((size_t)32, n - k0);
+    asm volatile(
+        "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra W_%=;\n}" ::"r"(cf_smem(bar)),
+        "r"(phase)
+        : "memory");
+    float y[128];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float4 v = *reinterpret_cast<const float4*>(myrow + 4 * i);
+      y[4 * i] = v.x;
+      y[4 * i + 1] = v.y;
+      y[4 * i + 2] = v.z;
+      y[4 * i + 3] = v.w;
+    }
+    const bool live = lane < nk;
+
+    // ---- gamma: sequential fp64 sum of squares (codec.hpp:219-221) -----------
+    double g2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < 128; ++i) {
+      const double d = (double)y[i];
+      g2 = __fma_rn(d, d, g2);  // the square is exact: == g2 + d*d rounded once
+    }
+    const double gamma = __dsqrt_rn(g2);
+    const float gf = (float)gamma;  // codec.hpp:233
+    const double inv = __ddiv_rn(1.0, gamma > 1e-12 ? gamma : 1e-12);
+    const float c32 = (float)(inv * p.inv_sqrt_d);
+    // outside [2^-60, 2^60] the fp32 rotation could lose range: exact path
+    bool ok = live && gamma > 8.7e-19 && gamma < 1.1e18;
+
+    // ---- rotation in fp32: ur = H (s .* k) * c -------------------------------
+#pragma unroll
+    for (int i = 0; i < 128; ++i)
+      if ((p.sign_mask[i >> 5] >> (i & 31)) & 1u) y[i] = -y[i];
+#pragma unroll
+    for (int len = 1; len < 128; len <<= 1)
+#pragma unroll
+      for (int i = 0; i < 128; ++i)
+        if (!(i & len)) {
+          const float a = y[i], b = y[i + len];
+          y[i] = a + b;
+          y[i + len] = a - b;
+        }
+#pragma unroll
+    for (int i = 0; i < 128; ++i) y[i] *= c32;
+
+    // the rotated row goes back to this lane's staging row; the triplet loop
+    // below is rolled (groups of 4 triplets = 3 float4) to keep the code small
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      *reinterpret_cast<float4*>(myrow + 4 * i) =
+          make_float4(y[4 * i], y[4 * i + 1], y[4 * i + 2], y[4 * i + 3]);
+
+    // ---- per-triplet joint rounding with certified decisions ----------------
+    // record bitstream writers into this lane's scratch words (LSB-first,
+    // codec.hpp:381-389): direction fields from bit 32, norm fields from bit
+    // 32 + 8 * dir_bytes
+    uint32_t* scr = scratch + lane;  // word i at scr[32 * i] (lane-interleaved)
+#pragma unroll
+    for (int i = 0; i <= S::RW; ++i) scr[32 * i] = 0u;
+    scr[0] = __float_as_uint(gf);
+    uint64_t dacc = 0, nacc = 0;
+    int dn = 0, nn = (8 * S::DIRB) & 31, dw = 1, nw = (32 + 8 * S::DIRB) >> 5;
+    auto put = [&](int wi, uint32_t v) { scr[32 * wi] |= v; };
+#pragma unroll 1
+    for (int q = 0; q < 11; ++q) {
+      float e[12];
+      {
+        const float4 v0 = *reinterpret_cast<const float4*>(myrow + 12 * q);
+        const float4 v1 = *reinterpret_cast<const float4*>(myrow + 12 * q + 4);
+        const float4 v2 = q < 10 ? *reinterpret_cast<const float4*>(myrow + 12 * q + 8)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+        e[0] = v0.x; e[1] = v0.y; e[2] = v0.z; e[3] = v0.w;
+        e[4] = v1.x; e[5] = v1.y; e[6] = v1.z; e[7] = v1.w;
+        e[8] = v2.x; e[9] = v2.y; e[10] = v2.z; e[11] = v2.w;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int t = 4 * q + j;
+        if (t >= S::NT) break;
+        const bool pad = t == S::NT - 1;  // elements 126, 127 and the zero pad
+        const float t0 = e[3 * j], t1 = e[3 * j + 1], t2 = pad ? 0.f : e[3 * j + 2];
+        const float a0 = fabsf(t0), a1 = fabsf(t1), a2 = fabsf(t2);
+        const float l1 = a0 + a1 + a2;
+        float il;  // rcp.approx: relative error <= 2^-23
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(il) : "f"(l1));
+        // |d xi| <= (|dt0| + |xi| |dl1|) / l1 + rounding <= 4 E0 / l1 + 5u
+        const float gx = 4.f * E0 * il * 1.001f + 6.f * U;
+        const bool up = pad || t2 >= 0.f;  // octahedral.hpp:28 (pad: pz = 0 exactly)
+        // hemisphere and, below it, sgn(px), sgn(py) (octahedral.hpp:29-30)
+        ok = ok && l1 > 1e-6f && (pad || a2 > E0) && (up || (a0 > E0 && a1 > E0));
+        const float xi = up ? t0 * il : copysignf(1.f - a1 * il, t0);
+        const float eta = up ? t1 * il : copysignf(1.f - a0 * il, t1);
+        const uint32_t sx = cf_bucket(xi, gx, mylut, ok);
+        const uint32_t sy = cf_bucket(eta, gx, mylut, ok);
+        uint32_t ix = sx, iy = sy;
+        float rv, gr;
+        if (MODE == 0) {  // scalar: rho of clamp(|t|, 0, 1) (codec.hpp:154-162)
+          rv = sqrtf(fmaf(t2, t2, fmaf(t1, t1, t0 * t0)));
+          gr = 1.7321f * E0 + 4.f * U;
+        } else {  // local3x3 (codec.hpp:164-192): strict '>' argmax over the window
+          float b1 = -INFINITY, b2 = -INFINITY;
+          uint32_t wi = 0;
+          // window corner (sx - 1, sy - 1) = padded cell (sx, sy)
+          const float4* wp = dtab + (sx * S::KP + sy) * S::DREP;
+#pragma unroll
+          for (int da = 0; da < 3; ++da)
+#pragma unroll
+            for (int db = 0; db < 3; ++db) {
+              const float4 nv = wp[(da * S::KP + db) * S::DREP];
+              const float sc = fmaf(t2, nv.z, fmaf(t1, nv.y, fmaf(t0, nv.x, nv.w)));
+              const bool gt = sc > b1;
+              b2 = fmaxf(b2, fminf(b1, sc));
+              b1 = fmaxf(b1, sc);
+              wi = gt ? (uint32_t)(da * 4 + db) : wi;
+            }
+          // score error: sqrt(3) E0 (rotation) + sqrt(3) u (fp32 table) + 3u (dot)
+          const float gs = 1.7321f * E0 + 5.f * U;
+          ok = ok && (b1 - b2 > 2.f * gs);
+          ix = sx + (wi >> 2) - 1;
+          iy = sy + (wi & 3) - 1;
+          rv = b1;
+          gr = gs;
+        }
+        rv = fminf(fmaxf(rv, 0.f), 1.f);
+        uint32_t ir = 0;
+#pragma unroll
+        for (int i = 0; i < S::KR - 1; ++i) {
+          ir += rv >= rbnd[i] ? 1u : 0u;
+          ok = ok && fabsf(rv - rbnd[i]) > gr + U;
+        }
+        // ---- append the fields ------------------------------------------------
+        dacc |= (uint64_t)(ix | (iy << BD)) << dn;
+        dn += 2 * BD;
+        if (dn >= 32) {
+          put(dw++, (uint32_t)dacc);
+          dacc >>= 32;
+          dn -= 32;
+        }
+        nacc |= (uint64_t)ir << nn;
+        nn += BN;
+        if (nn >= 32) {
+          put(nw++, (uint32_t)nacc);
+          nacc >>= 32;
+          nn -= 32;
+        }
+      }
+    }
+    if (dn > 0) put(dw, (uint32_t)dacc);
+    if (nn > 0) put(nw, (uint32_t)nacc);
+    __syncwarp();
+    if (blk + wstride < nblk) {  // the staging row is consumed: fetch the next block
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      request(blk + wstride);
+    }
+    uint32_t w[S::RW + 1];
+#pragma unroll
+    for (int i = 0; i <= S::RW; ++i) w[i] = i < S::RW ? scr[32 * i] : 0u;
+
+    // ---- flagged keys: exact re-encode later --------------------------------
+    const uint32_t bad = __ballot_sync(kFull, live && !ok);
+    if (bad) {
+      uint32_t basei = 0;
+      if (lane == 0) basei = atomicAdd(flag_cnt, (uint32_t)__popc(bad));
+      basei = __shfl_sync(kFull, basei, 0);
+      if (live && !ok) flag_idx[basei + __popc(bad & ((1u << lane) - 1u))] = (uint32_t)(k0 + lane);
+    }
+
+    // ---- the warp's 32 records -> shared buffer -> one bulk store ------------
+    {
+      const uint32_t D = (uint32_t)lane * S::RB, o = 8 * (D & 3), wb = D >> 2;
+      const uint32_t last = (D + S::RB - 1) >> 2;  // last word this record touches
+      uint32_t prev = 0, mine[S::RW + 1];
+#pragma unroll
+      for (int j = 0; j <= S::RW; ++j) {
+        mine[j] = o ? __funnelshift_l(prev, w[j], o) : w[j];
+        prev = w[j];
+      }
+      // the first word may share bytes with lane-1's last word
+      const uint32_t up = __shfl_up_sync(kFull, (last - wb == S::RW) ? mine[S::RW] : mine[S::RW - 1], 1);
+      const uint32_t prev_last = __shfl_up_sync(kFull, last, 1);
+      if (lane > 0 && prev_last == wb) mine[0] |= up;
+      const bool share_end = lane < 31 && ((D + S::RB) & 3);
+#pragma unroll
+      for (int j = 0; j <= S::RW; ++j) {
+        const uint32_t wd = wb + j;
+        if (wd < last || (wd == last && !share_end)) wrec[wd] = mine[j];
+      }
+    }
+    __syncwarp();
+    uint8_t* dst = out + k0 * S::RB;
+    if (nk == 32) {
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                     "r"(cf_smem(wrec)), "r"(32 * S::RB)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+    } else {
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(wrec);
+      for (int i = lane; i < nk * S::RB; i += 32) dst[i] = src[i];
+    }
+    __syncwarp();
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <int BD, int BN, int MODE>
+static cudaError_t launch_cf(const OqCodecParams& p, const float* x, size_t n, uint8_t* out,
+                             uint32_t* flag_idx, uint32_t* flag_cnt, cudaStream_t st,
+                             int num_sms) {
+  using S = CFS<BD, BN>;
+  cudaError_t e = cudaFuncSetAttribute(compress_fast_kernel<BD, BN, MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+  if (e != cudaSuccess) return e;
+  const size_t nblk = (n + 31) / 32;
+  size_t grid = (nblk + kCFWarps - 1) / kCFWarps;
+  if (grid > (size_t)num_sms) grid = num_sms;
+  compress_fast_kernel<BD, BN, MODE>
+      <<<(unsigned)grid, kCFThreads, S::SMEM, st>>>(p, x, n, out, flag_idx, flag_cnt);
+  return cudaGetLastError();
+}
+
+bool compress_fast_ok(const OqCodecParams& p, int dtype, const void* x, const void* out) {
+  if (p.dim != 128 || p.qjl || dtype != OQ_F32) return false;
+  if (p.rounding != 0 && p.rounding != 2) return false;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(out) & 15)) return false;
+  return (p.b_dir == 3 && p.b_nrm == 1) || (p.b_dir == 4 && p.b_nrm == 2) ||
+         (p.b_dir == 5 && p.b_nrm == 3);
+}
+
+cudaError_t launch_compress_fast(const OqCodecParams& p, const float* x, size_t n, uint8_t* out,
+                                 uint32_t* flag_idx, uint32_t* flag_cnt, cudaStream_t st,
+                                 int num_sms) {
+#define OQ_CF(BD, BN)                                                                      \
+  if (p.b_dir == BD && p.b_nrm == BN)                                                      \
+    return p.rounding == 0 ? launch_cf<BD, BN, 0>(p, x, n, out, flag_idx, flag_cnt, st, num_sms) \
+                           : launch_cf<BD, BN, 2>(p, x, n, out, flag_idx, flag_cnt, st, num_sms);
+  OQ_CF(3, 1)
+  OQ_CF(4, 2)
+  OQ_CF(5, 3)
+#undef OQ_CF
+  return cudaErrorNotSupported;
+}
+
+}  // namespace oqd

@@ -8,9 +8,17 @@
 
 namespace oqd {
 
-// K1: Encoder::encode -> OCTO v1 records.
+// K1: Encoder::encode -> OCTO v1 records.  d = 128 fp32 keys at the BASELINE
+// bit splits take the certified fp32 pass (compress_fast.cu) and re-encode
+// the keys it flags exactly; `flagged` (device u32, optional) receives how
+// many keys took the exact path.
 cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, size_t n,
-                            uint8_t* out, cudaStream_t st, int num_sms);
+                            uint8_t* out, cudaStream_t st, int num_sms,
+                            uint32_t* flagged = nullptr);
+bool compress_fast_ok(const OqCodecParams& p, int dtype, const void* x, const void* out);
+cudaError_t launch_compress_fast(const OqCodecParams& p, const float* x, size_t n, uint8_t* out,
+                                 uint32_t* flag_idx, uint32_t* flag_cnt, cudaStream_t st,
+                                 int num_sms);
 // K2: Encoder::decode of OCTO v1 records -> fp32 [n, dim].
 cudaError_t launch_decode(const OqCodecParams& p, const uint8_t* recs, size_t n, float* out,
                           cudaStream_t st, int num_sms);
