@@ -142,6 +142,16 @@ oq_status build_codec(const oq_config* cfg, const oqh::Book& xi, const oqh::Book
   c->cfg = *cfg;
   c->device = dev;
   c->num_sms = nsm;
+  {
+    // K1's stream-ordered workspace (flagged-key list) comes from the
+    // device's default pool: keep freed blocks cached instead of returning
+    // them to the driver at every synchronisation.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = 1ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   c->xi_c = xi.centroids;
   c->rho_c = rho.centroids;
   OqCodecParams& p = c->p;

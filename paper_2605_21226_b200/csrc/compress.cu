@@ -504,8 +504,24 @@ static cudaError_t launch_compress_d(const OqCodecParams& p, const void* x, int 
 cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, size_t n,
                             uint8_t* out, cudaStream_t st, int num_sms, uint32_t* flagged) {
   if (n == 0) return cudaSuccess;
-  if (compress_fast_ok(p, dtype, x, out) && !getenv("OQ_COMPRESS_EXACT")) {
-    // certified fp32 pass, then the exact kernel over the keys it flagged
+  // d = 128 fp32 keys at the BASELINE bit splits: the single-pass two-lanes-
+  // per-key kernel (compress_x2.cu) unless OQ_COMPRESS_IMPL selects the
+  // certified-fp32 pass + exact re-encode ("fast") or the generic exact
+  // kernel ("exact") for comparison runs.
+  static const int impl = [] {
+    const char* e = getenv("OQ_COMPRESS_IMPL");
+    if (!e) return 1;
+    return e[0] == 'x' ? 0 : (e[0] == 'e' ? 2 : 1);
+  }();
+  if (impl == 0 && compress_fast_ok(p, dtype, x, out)) {
+    cudaError_t e = flagged ? cudaMemsetAsync(flagged, 0, sizeof(uint32_t), st) : cudaSuccess;
+    if (e == cudaSuccess)
+      e = launch_compress_x2(p, static_cast<const float*>(x), n, out, st, num_sms);
+    return e;
+  }
+  if (impl == 1 && compress_fast_ok(p, dtype, x, out)) {
+    // certified fp32 pass, then the exact two-lanes-per-key kernel over the
+    // keys it flagged
     uint32_t* ws = nullptr;
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), (n + 4) * sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
@@ -513,7 +529,7 @@ cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, si
     if (e == cudaSuccess)
       e = launch_compress_fast(p, static_cast<const float*>(x), n, out, ws + 4, ws, st, num_sms);
     if (e == cudaSuccess)
-      e = launch_compress_d<128>(p, x, dtype, n, out, st, num_sms, ws + 4, ws);
+      e = launch_compress_x2(p, static_cast<const float*>(x), n, out, st, num_sms, ws + 4, ws);
     if (e == cudaSuccess && flagged)
       e = cudaMemcpyAsync(flagged, ws, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
     const cudaError_t f = cudaFreeAsync(ws, st);
