@@ -132,6 +132,9 @@ size_t oq_cache_bytes(const oq_codec* codec, int role, uint64_t tokens); /* per 
 oq_status oq_cache_pack(const oq_codec* codec, int role, const void* records, uint64_t n_streams,
                         uint64_t n_tokens, uint64_t rec_stride_tokens, void* tiles,
                         uint64_t cap_tokens, void* stream);
+/* Device scratch for the attention calls.  Its first 64 KiB hold per-stream
+ * arrival counters: they must be zero when the workspace is first used (the
+ * kernels leave them zero), so allocate it zero-filled. */
 size_t oq_attention_workspace_bytes(const oq_codec* ck, const oq_codec* cv,
                                     const oq_attn_shape* shape, int n_splits);
 oq_status oq_attention_decode(const oq_codec* ck, const oq_codec* cv, const oq_attn_shape* shape,

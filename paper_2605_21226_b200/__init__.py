@@ -434,7 +434,9 @@ class _Workspace:
         key = str(device)
         b = cls.buf.get(key)
         if b is None or b.numel() < nbytes:
-            b = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            # zeroed once: the attention kernels keep their arrival counters
+            # (the first 64 KiB) at zero between calls
+            b = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
             cls.buf[key] = b
         return b
 

@@ -177,6 +177,25 @@ __device__ __forceinline__ uint32_t sign_pair(uint32_t nw, int sigma) {
   return ((nw << (15 - sigma)) & 0x80008000u) | 0x3C003C00u;
 }
 
+__device__ __forceinline__ void wht128_lane4(float (&y)[4], int lane) {
+  // normalized-free WHT over 128 values, 4 consecutive per lane
+  {
+    const float a = y[0], b = y[1], c2 = y[2], d = y[3];
+    y[0] = a + b; y[1] = a - b; y[2] = c2 + d; y[3] = c2 - d;
+    const float e0 = y[0], e1 = y[1];
+    y[0] = e0 + y[2]; y[1] = e1 + y[3]; y[2] = e0 - y[2]; y[3] = e1 - y[3];
+  }
+#pragma unroll
+  for (int lm = 1; lm < 32; lm <<= 1) {
+    const bool up = lane & lm;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float o = __shfl_xor_sync(kFull, y[i], lm);
+      y[i] = up ? o - y[i] : y[i] + o;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 struct AttnKParams {
   const uint2* tab;  // global joint table (2^W entries)
@@ -193,6 +212,15 @@ struct AttnKParams {
   // [tb0, tb0 + tps) are cut into gridDim.x equal contiguous ranges.
   int streamk, n_sh;
   size_t tb0, tps;
+  // fused mode (single-GPU attention_decode): the kernel prepares the query
+  // fragments itself from q and finalises each stream's rows once its last
+  // partial lands (per-stream arrival counters, left at zero)
+  int fuse, qjl;
+  const float* q;        // [B, Hq, 128]
+  float* out;            // [B * Hq, 128]
+  uint32_t* counters;    // [n_sh], zero on entry and exit
+  uint32_t smask[4], qmask[4], vmask[4];
+  float inv_sqrt_d;
 };
 
 template <int W, bool QJL>
@@ -204,7 +232,8 @@ struct Cfg {
   static constexpr int VTILE = (128 + 4 * VCODE + 15) & ~15;
   static constexpr int QF = 18 + (QJL ? 16 : 0);
   static constexpr int TAB_BYTES = (1 << W) * 16 * 8;
-  static constexpr int smem(int nw) { return TAB_BYTES + nw * 8 * kPartW * 4; }
+  static constexpr int QS_FLOATS = 8 * 2 * 129;  // fused query prep scratch
+  static constexpr int smem(int nw) { return TAB_BYTES + nw * 8 * kPartW * 4 + QS_FLOATS * 4; }
 };
 
 template <int W, bool QJL>
@@ -530,6 +559,102 @@ __device__ __forceinline__ void merge_store(const AttnKParams& P, const Seg& it,
   }
 }
 
+// Fused K5 for one segment's (stream, head chunk): warp w rotates head
+// 8 hc + w of q (Encoder::prepare, codec.hpp:282-292) into smem, then every
+// lane gathers its mma B fragments (same layout as qprep_kernel).
+template <int QF>
+__device__ __forceinline__ void seg_qprep(uint32_t (&qf)[QF], const AttnKParams& P, int sh,
+                                          float* qs, int warp, int nwarps, int lane) {
+  const int hc = sh % P.HC, stream = sh / P.HC;
+  const int b = stream / P.Hkv, kvh = stream % P.Hkv;
+  const float log2e = 1.4426950408889634f;
+  for (int w = warp; w < 8; w += nwarps) {
+    float* qsw = qs + w * 129;
+    float* qkw = qs + (8 + w) * 129;
+    const int h = 8 * hc + w;
+    if (h < P.G) {
+      const float* q = P.q + ((size_t)b * P.Hq + (size_t)kvh * P.G + h) * 128;
+      const float4 q4 = __ldg(reinterpret_cast<const float4*>(q) + lane);
+      float y[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = 4 * lane + i;
+        if ((P.smask[e >> 5] >> (e & 31)) & 1u) y[i] = -y[i];
+      }
+      wht128_lane4(y, lane);
+      const float s_attn = P.inv_sqrt_d * P.inv_sqrt_d * log2e;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) qsw[4 * lane + i] = y[i] * s_attn;
+      if (P.qjl) {
+        float z[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int e = 4 * lane + i;
+          const float v = y[i] * P.inv_sqrt_d;
+          z[i] = ((P.qmask[e >> 5] >> (e & 31)) & 1u) ? -v : v;
+        }
+        wht128_lane4(z, lane);
+        const float s_sk = P.inv_sqrt_d * P.inv_sqrt_d * log2e * sqrtf(1.5707963267948966f / 128.f);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) qkw[4 * lane + i] = z[i] * s_sk;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) qsw[4 * lane + i] = qkw[4 * lane + i] = 0.f;
+    }
+  }
+  __syncthreads();
+  const int g = lane >> 2, c = lane & 3;
+#pragma unroll
+  for (int sigma = 0; sigma < 18; ++sigma) {
+    int d0, d1;
+    k_slot_dims(c, sigma, d0, d1);
+    qf[sigma] = pack_h2(d0 >= 0 ? qs[g * 129 + d0] : 0.f, d1 >= 0 ? qs[g * 129 + d1] : 0.f);
+  }
+  if (QF > 18)
+#pragma unroll
+    for (int sigma = 0; sigma < 16; ++sigma)
+      qf[18 + sigma] = pack_h2(qs[(8 + g) * 129 + 32 * c + sigma],
+                               qs[(8 + g) * 129 + 32 * c + sigma + 16]);
+}
+
+// Fused K4 for one row: merge its n partials in order (SoftmaxState::merge,
+// attention.hpp:36-44), acc / l, inverse V rotation; one warp.
+__device__ __forceinline__ void combine_row(const float* base, int n, float* out,
+                                            const uint32_t (&vmask)[4], float inv_sqrt_d,
+                                            int lane) {
+  const float NEG_INF = -__int_as_float(0x7f800000);
+  float M = NEG_INF;
+  for (int i = lane; i < n; i += 32) {
+    const float2 ml = *reinterpret_cast<const float2*>(base + (size_t)i * kPartW);
+    if (ml.y > 0.f) M = fmaxf(M, ml.x);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
+  float L = 0.f, y[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < n; ++i) {
+    const float2 ml = *reinterpret_cast<const float2*>(base + (size_t)i * kPartW);
+    if (ml.y > 0.f) {
+      const float f = ex2(ml.x - M);
+      L += ml.y * f;
+      const float4 a4 = *reinterpret_cast<const float4*>(base + (size_t)i * kPartW + 4 + 4 * lane);
+      y[0] += a4.x * f; y[1] += a4.y * f; y[2] += a4.z * f; y[3] += a4.w * f;
+    }
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) y[i] *= inv;
+  wht128_lane4(y, lane);
+  float r[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int e = 4 * lane + i;
+    const float v = y[i] * inv_sqrt_d;
+    r[i] = ((vmask[e >> 5] >> (e & 31)) & 1u) ? -v : v;
+  }
+  *reinterpret_cast<float4*>(out + 4 * lane) = make_float4(r[0], r[1], r[2], r[3]);
+}
+
 // Variant A: each warp streams its tiles from HBM straight into registers,
 // prefetching one tile ahead (ping-pong register images).
 template <int W, bool QJL, int kAttnWarps>
@@ -538,6 +663,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
   uint8_t* smem = g_attn_smem;
   uint2* tab = reinterpret_cast<uint2*>(smem);
   float* merge = reinterpret_cast<float*>(smem + C::TAB_BYTES);
+  float* qs = merge + kAttnWarps * 8 * kPartW;
+  __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, c = lane & 3;
 
@@ -546,14 +673,16 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
       static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + ((lane & 15) << 3);
   __syncthreads();
 
-  auto run = [&](const Seg& it) {
-    uint32_t qf[C::QF];
-    load_qfrag(qf, P, it.sh, lane);
-    WarpState S;
-    init_state(S);
+  auto run = [&](const Seg& it, int nparts) {
     TileRegs<W, QJL> ra, rb;
     size_t tile = it.tlo + warp;
+    // first tile in flight while the query fragments are prepared
     if (tile < it.thi) load_tile<W, QJL>(ra, P, it.stream, tile, g, c, lane, lane);
+    uint32_t qf[C::QF];
+    if (P.fuse) seg_qprep(qf, P, it.sh, qs, warp, kAttnWarps, lane);
+    else load_qfrag(qf, P, it.sh, lane);
+    WarpState S;
+    init_state(S);
     while (tile < it.thi) {
       size_t tn = tile + kAttnWarps;
       if (tn < it.thi) load_tile<W, QJL>(rb, P, it.stream, tn, g, c, lane, lane);
@@ -568,19 +697,41 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
     warp_state_out(S, merge + warp * 8 * kPartW, g, c);
     __syncthreads();
     merge_store<kAttnWarps>(P, it, merge, tid, blockDim.x);
+    if (P.fuse) {
+      // the CTA that lands a stream's last partial finalises its rows
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        const uint32_t old = atomicAdd(&P.counters[it.sh], 1u);
+        s_last = old + 1 == (uint32_t)nparts;
+        if (s_last) P.counters[it.sh] = 0u;
+      }
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        for (int w = warp; w < 8; w += kAttnWarps) {
+          if (8 * it.hc + w >= P.G) continue;
+          const size_t row = (size_t)it.b * P.Hq + (size_t)it.kvh * P.G + 8 * it.hc + w;
+          combine_row(P.partials + row * P.n_parts * kPartW, nparts, P.out + row * 128, P.vmask,
+                      P.inv_sqrt_d, lane);
+        }
+      }
+    }
     __syncthreads();
   };
 
   if (!P.streamk) {
-    for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) run(item_seg(P, item));
+    for (int item = blockIdx.x; item < P.n_items; item += gridDim.x)
+      run(item_seg(P, item), P.splits);
   } else {
     const size_t U = (size_t)P.n_sh * P.tps, G = gridDim.x;
     const size_t u0 = sk_bound(blockIdx.x, U, G), u1 = sk_bound(blockIdx.x + 1, U, G);
     for (size_t sh = u0 / P.tps; sh * P.tps < u1; ++sh) {
       const size_t s0 = sh * P.tps, s1 = s0 + P.tps;
       const size_t a = max(u0, s0), z = min(u1, s1);
-      const int part = (int)blockIdx.x - sk_cta(s0, U, G);
-      run(make_seg(P, (int)sh, P.tb0 + (a - s0), P.tb0 + (z - s0), part, z == s1));
+      const int first = sk_cta(s0, U, G), part = (int)blockIdx.x - first;
+      run(make_seg(P, (int)sh, P.tb0 + (a - s0), P.tb0 + (z - s0), part, z == s1),
+          sk_cta(s1 - 1, U, G) - first + 1);
     }
   }
 }
@@ -597,25 +748,6 @@ struct QPrepParams {
   float inv_sqrt_d;
   int qjl;
 };
-
-__device__ __forceinline__ void wht128_lane4(float (&y)[4], int lane) {
-  // normalized-free WHT over 128 values, 4 consecutive per lane
-  {
-    const float a = y[0], b = y[1], c2 = y[2], d = y[3];
-    y[0] = a + b; y[1] = a - b; y[2] = c2 + d; y[3] = c2 - d;
-    const float e0 = y[0], e1 = y[1];
-    y[0] = e0 + y[2]; y[1] = e1 + y[3]; y[2] = e0 - y[2]; y[3] = e1 - y[3];
-  }
-#pragma unroll
-  for (int lm = 1; lm < 32; lm <<= 1) {
-    const bool up = lane & lm;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float o = __shfl_xor_sync(kFull, y[i], lm);
-      y[i] = up ? o - y[i] : y[i] + o;
-    }
-  }
-}
 
 __global__ void qprep_kernel(QPrepParams P) {
   __shared__ float qs[8][129];
@@ -900,6 +1032,17 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
     const size_t tz = (te + kTileTok - 1) / kTileTok;
     P.tps = tz > P.tb0 ? tz - P.tb0 : 0;
   }
+  P.fuse = a.out != nullptr && a.counters != nullptr;
+  P.qjl = pk.qjl;
+  P.q = a.q;
+  P.out = a.out;
+  P.counters = a.counters;
+  for (int i = 0; i < 4; ++i) {
+    P.smask[i] = pk.sign_mask[i];
+    P.qmask[i] = pk.qsign_mask[i];
+    P.vmask[i] = a.vmask[i];
+  }
+  P.inv_sqrt_d = (float)pk.inv_sqrt_d;
   int grid = P.n_items < num_sms ? P.n_items : num_sms;
   if (P.streamk) {
     const size_t U = (size_t)P.n_sh * P.tps;

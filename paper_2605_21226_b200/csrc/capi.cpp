@@ -460,6 +460,10 @@ static int parts_per_row(const oq_codec* ck, const oq_attn_shape* sh, uint64_t t
   return oqd::attention_num_parts(sh->B, sh->Hq, sh->Hkv, sh->T, t0, t1, n_splits, ck->num_sms);
 }
 
+// Workspace layout: [per-stream arrival counters, 64 KiB: zero on first use,
+// the fused kernel leaves them zero][partials][query fragments].
+static constexpr size_t kCounterBytes = 64 * 1024;
+
 size_t oq_attention_workspace_bytes(const oq_codec* ck, const oq_codec* cv,
                                     const oq_attn_shape* sh, int n_splits) {
   if (!ck || !cv || !sh || n_splits < 0 || sh->Hkv < 1) return 0;
@@ -469,7 +473,7 @@ size_t oq_attention_workspace_bytes(const oq_codec* ck, const oq_codec* cv,
   const size_t part = rows * np * (4 + ck->cfg.dim) * sizeof(float);
   const size_t hc = sh->Hkv > 0 ? (size_t)((sh->Hq / sh->Hkv + 7) / 8) : 1;
   const size_t qf = (size_t)sh->B * sh->Hkv * hc * oqd::attention_qfrag_bytes(ck->p);
-  return ((part + 255) & ~size_t(255)) + qf + 256;
+  return kCounterBytes + ((part + 255) & ~size_t(255)) + qf + 256;
 }
 
 static oq_status attn_check(const oq_codec* ck, const oq_codec* cv, const oq_attn_shape* sh,
@@ -495,11 +499,12 @@ static oq_status attn_check(const oq_codec* ck, const oq_codec* cv, const oq_att
 static oq_status run_partials(const oq_codec* ck, const oq_codec* cv, const oq_attn_shape* sh,
                               const float* q, const void* kc, const void* vc, uint64_t t0,
                               uint64_t t1, int n_splits, void* ws, cudaStream_t st,
-                              float** parts_out, int* n_parts_out) {
+                              float** parts_out, int* n_parts_out, float* fused_out = nullptr) {
   const size_t rows = (size_t)sh->B * sh->Hq;
   const int np_max = parts_per_row(ck, sh, 0, sh->T, n_splits) + 1;
   const int np = parts_per_row(ck, sh, t0, t1, n_splits);
   const size_t part = rows * (size_t)np_max * (4 + ck->cfg.dim) * sizeof(float);
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
   oqd::AttnArgs a{};
   a.B = sh->B;
   a.Hq = sh->Hq;
@@ -512,18 +517,29 @@ static oq_status run_partials(const oq_codec* ck, const oq_codec* cv, const oq_a
   a.kcache = static_cast<const uint8_t*>(kc);
   a.vcache = static_cast<const uint8_t*>(vc);
   a.k_tiles_cap = a.v_tiles_cap = (sh->cap_tokens + 31) / 32;
-  a.partials = static_cast<float*>(ws);
+  a.partials = reinterpret_cast<float*>(w8 + kCounterBytes);
   a.n_parts = np;
   *n_parts_out = np;
-  a.qfrag = static_cast<uint8_t*>(ws) + ((part + 255) & ~size_t(255));
-  cudaError_t e = oqd::launch_qprep(ck->p, a, st);
-  if (e != cudaSuccess) return cuda_fail(e, "qprep kernel");
+  a.qfrag = w8 + kCounterBytes + ((part + 255) & ~size_t(255));
+  // one launch when the per-stream counters fit: q prep and the final merge
+  // run inside the attention kernel
+  const size_t n_sh = (size_t)sh->B * sh->Hkv * ((sh->Hq / sh->Hkv + 7) / 8);
+  const bool fuse = fused_out && n_sh * 4 <= kCounterBytes && !getenv("OQ_ATTN_UNFUSED");
+  cudaError_t e = cudaSuccess;
+  if (fuse) {
+    a.out = fused_out;
+    a.counters = reinterpret_cast<uint32_t*>(w8);
+    for (int i = 0; i < 4; ++i) a.vmask[i] = cv->p.sign_mask[i];
+  } else {
+    e = oqd::launch_qprep(ck->p, a, st);
+    if (e != cudaSuccess) return cuda_fail(e, "qprep kernel");
+  }
   {
     TimedScope ts("attention", st);
     e = oqd::launch_attention_partials(ck->p, cv->p, a, n_splits, st, ck->num_sms);
   }
   if (e != cudaSuccess) return cuda_fail(e, "attention kernel");
-  *parts_out = a.partials;
+  *parts_out = fuse ? nullptr : a.partials;
   return OQ_OK;
 }
 
@@ -535,8 +551,10 @@ oq_status oq_attention_decode(const oq_codec* ck, const oq_codec* cv, const oq_a
   if (!out || !ws) return fail(OQ_ERR_INVALID_ARGUMENT, "null argument");
   float* parts = nullptr;
   int np = 0;
-  s = run_partials(ck, cv, sh, q, kc, vc, 0, sh->T, n_splits, ws, as_stream(stream), &parts, &np);
+  s = run_partials(ck, cv, sh, q, kc, vc, 0, sh->T, n_splits, ws, as_stream(stream), &parts, &np,
+                   out);
   if (s) return s;
+  if (!parts) return OQ_OK;  // fused: the attention kernel wrote out
   const int rows = sh->B * sh->Hq;
   const size_t w = 4 + ck->cfg.dim;
   cudaError_t e = oqd::launch_attention_combine(cv->p, parts, rows, np, np * w, w, 1,

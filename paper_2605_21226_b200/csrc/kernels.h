@@ -44,6 +44,10 @@ struct AttnArgs {
   int n_parts;           // split-K partial slots per (b, q head)
   float* out;            // [B, Hq, D] fp32 (combine output)
   void* qfrag;           // [B*Hkv] fragment scratch (attention_qfrag_bytes each)
+  // fused single-launch mode (attention_decode on one GPU): when both are set
+  // the attention kernel prepares q itself and writes the final rows to out
+  uint32_t* counters = nullptr;  // [B*Hkv*ceil(G/8)] zero on entry, left zero
+  uint32_t vmask[4] = {0, 0, 0, 0};  // V rotation signs (for the fused combine)
 };
 
 size_t attention_tile_bytes(const OqCodecParams& p, int role);  // role 0 = K, 1 = V
