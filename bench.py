@@ -52,6 +52,20 @@ def rec_bytes(bits, qjl):
     return r + (18 if qjl else 0)
 
 
+def ncu_traffic(kernel_prefix):
+    """DRAM bytes per launch of a kernel from the committed ncu --set full capture
+    (profiles/ncu_traffic.json, written by tools/ncu_summary.py traffic), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)["dram_bytes_per_launch"]
+    except Exception:
+        return None
+    for k, v in d.items():
+        if k.startswith(kernel_prefix):
+            return v
+    return None
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -383,7 +397,9 @@ def main():
             "config": workload_config(args, world, splits),
             "hbm_frac_of_peak": value / world / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+                         "frac": achieved / peak, "peak_kind": peak_kind,
+                         "traffic": ncu_traffic(f"attn_partials_kernel<{3 * bits + 1}, {int(qjl)}, 8>"),
+                         "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/)",
                          "kernel": "attn_partials_kernel (K3)",
                          "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": alg_bytes_rank},
             "cpu_baseline": cpu,
@@ -392,7 +408,9 @@ def main():
                     "what": "pinned q H2D + public-API attention + out D2H per step; KV cache "
                             "device-resident"},
             "clocks": clk.summary(),
-            "gpu_launches": (3 if world == 1 else 3) * args.steps,
+            # world 1: one fused K3 launch per step; sharded: K5 + K3 + local
+            # merge + final merge around the NCCL all-gather
+            "gpu_launches": (1 if world == 1 else 4) * args.steps,
             "compress": comp,
         }
         print(json.dumps(line), flush=True)

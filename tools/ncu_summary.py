@@ -63,67 +63,107 @@ def launches(path):
     print("| kernel | launches | mean us |\n|---|---|---|")
     for n, (c, t) in agg.items():
         print(f"| `{n}` | {c} | {t / c:.1f} |")
-    # last decode step = last qprep .. combine window
-    idx = [i for i, (n, _) in enumerate(seq) if "qprep" in n]
+    # last decode step: the last attention launch with its qprep / combine
+    # neighbours (the fused path has neither)
+    idx = [i for i, (n, _) in enumerate(seq) if "attn_partials" in n]
     if idx:
         i0 = idx[-1]
-        step = [(n, t) for n, t in seq[i0:i0 + 3]]
+        lo = i0 - 1 if i0 > 0 and "qprep" in seq[i0 - 1][0] else i0
+        hi = i0 + 2 if i0 + 1 < len(seq) and "combine" in seq[i0 + 1][0] else i0 + 1
+        step = seq[lo:hi]
         tot = sum(t for _, t in step)
         print("\nLast decode step (cold-cache, serialised under ncu):")
         for n, t in step:
             print(f"- `{n}`: {t:.1f} us ({100 * t / tot:.1f} % of the step)")
 
 
+def traffic(path):
+    """{kernel: dram read + write bytes per launch} of a --set full report."""
+    raw = _csv(["-i", path, "--page", "raw", "--csv"])
+    h, units = raw[0], raw[1]
+    out = {}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for v in raw[2:]:
+        name = v[h.index("Kernel Name")].split("(")[0].replace("void ", "")
+        b = 0.0
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = h.index(key)
+            b += float(v[i].replace(",", "")) * scale.get(units[i], 1)
+        out[name] = b
+    return out
+
+
+def _sass_sections(src):
+    """Split the --page source csv (one section per kernel) into row lists."""
+    secs, cur = [], None
+    for r in src:
+        if r and r[0] == "Kernel Name":
+            cur = {"name": r[1] if len(r) > 1 else "", "rows": []}
+            secs.append(cur)
+        elif cur is not None:
+            cur["rows"].append(r)
+    return secs
+
+
 def full(path, units, unit_name):
     raw = _csv(["-i", path, "--page", "raw", "--csv"])
-    h, v = raw[0], raw[2]
-    print(f"Kernel: `{v[h.index('Kernel Name')]}`\n")
-    print("| counter | value |\n|---|---|")
-    for k in RAW_KEYS:
-        if k in h:
-            print(f"| {k} ({raw[1][h.index(k)]}) | {v[h.index(k)]} |")
-    print("\nStalls per issued instruction (> 0.05):\n")
-    for i, n in enumerate(h):
-        if "issue_stalled" in n and "per_issue_active" in n:
-            try:
-                if float(v[i]) > 0.05:
-                    print(f"- {n.split('stalled_')[1].split('_per')[0]}: {float(v[i]):.2f}")
-            except ValueError:
-                pass
+    h = raw[0]
     src = _csv(["-i", path, "--page", "source", "--csv", "--print-source", "sass"])
-    hdr, data = src[1], src[2:]
-    si, ei = hdr.index("Source"), hdr.index("Instructions Executed")
-    ss = hdr.index("Warp Stall Sampling (All Samples)")
-    cnt, stl, tot, stot = Counter(), Counter(), 0, 0
-    for r in data:
-        try:
-            n = int(r[ei].replace(",", ""))
-        except ValueError:
+    secs = _sass_sections(src)
+    for k, v in enumerate(raw[2:]):
+        print(f"### `{v[h.index('Kernel Name')]}`\n")
+        print("| counter | value |\n|---|---|")
+        for key in RAW_KEYS:
+            if key in h:
+                print(f"| {key} ({raw[1][h.index(key)]}) | {v[h.index(key)]} |")
+        print("\nStalls per issued instruction (> 0.05):\n")
+        for i, n in enumerate(h):
+            if "issue_stalled" in n and "per_issue_active" in n:
+                try:
+                    if float(v[i]) > 0.05:
+                        print(f"- {n.split('stalled_')[1].split('_per')[0]}: {float(v[i]):.2f}")
+                except ValueError:
+                    pass
+        if k >= len(secs):
             continue
-        op = re.sub(r"^@!?U?P\w+\s+", "", r[si].strip())
-        op = op.split()[0] if op else "?"
-        cnt[op] += n
-        tot += n
-        s = int(r[ss] or 0)
-        stl[op] += s
-        stot += s
-    per = f"per {unit_name}" if units else "total"
-    div = units if units else 1
-    print(f"\nSASS mix (warp instructions {per}; total {tot / div:.1f}):\n")
-    print(f"| op | {per} | stall share |\n|---|---|---|")
-    for k, c in cnt.most_common(24):
-        print(f"| {k} | {c / div:.1f} | {100 * stl[k] / max(1, stot):.1f} % |")
+        rows = secs[k]["rows"]
+        hdr, data = rows[0], rows[1:]
+        si, ei = hdr.index("Source"), hdr.index("Instructions Executed")
+        ss = hdr.index("Warp Stall Sampling (All Samples)")
+        cnt, stl, tot, stot = Counter(), Counter(), 0, 0
+        for r in data:
+            try:
+                n = int(r[ei].replace(",", ""))
+            except (ValueError, IndexError):
+                continue
+            op = re.sub(r"^@!?U?P\w+\s+", "", r[si].strip())
+            op = op.split()[0] if op else "?"
+            cnt[op] += n
+            tot += n
+            sv = int(r[ss] or 0)
+            stl[op] += sv
+            stot += sv
+        per = f"per {unit_name}" if units else "total"
+        div = units if units else 1
+        print(f"\nSASS mix (warp instructions {per}; total {tot / div:.1f}):\n")
+        print(f"| op | {per} | stall share |\n|---|---|---|")
+        for op, c in cnt.most_common(16):
+            print(f"| {op} | {c / div:.1f} | {100 * stl[op] / max(1, stot):.1f} % |")
+        print()
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["launches", "full"])
+    ap.add_argument("mode", choices=["launches", "full", "traffic"])
     ap.add_argument("path")
     ap.add_argument("--units", type=float, default=0)
     ap.add_argument("--unit-name", default="unit")
     a = ap.parse_args()
     if a.mode == "launches":
         launches(a.path)
+    elif a.mode == "traffic":
+        import json
+        print(json.dumps(traffic(a.path), indent=1))
     else:
         full(a.path, a.units, a.unit_name)
 
