@@ -125,6 +125,15 @@ typedef struct oq_attn_shape {
   const int32_t* seq_lens;/* optional device [B] lengths (<= T), NULL = all T */
 } oq_attn_shape;
 
+/* Decode-step append (the step beside attention_decode in a decoder): compress
+ * one new vector per stream x [n_streams, dim] (Encoder::encode,
+ * codec.hpp:214-249) and write it into token slot pos of each stream's tiles
+ * (pos_dev: device int64 [n_streams], or NULL for the scalar pos), leaving the
+ * stream's other tokens untouched.  records: device scratch of
+ * n_streams * oq_record_bytes bytes that receives the OCTO records. */
+oq_status oq_cache_append(const oq_codec* codec, int role, const void* x, int dtype,
+                          uint64_t n_streams, const int64_t* pos_dev, int64_t pos, void* records,
+                          void* tiles, uint64_t cap_tokens, void* stream);
 size_t oq_cache_tile_bytes(const oq_codec* codec, int role); /* bytes per 32-token tile */
 size_t oq_cache_bytes(const oq_codec* codec, int role, uint64_t tokens); /* per stream */
 /* records: device [n_streams][rec_stride_tokens] records of n_tokens each

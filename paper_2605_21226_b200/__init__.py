@@ -94,6 +94,8 @@ def lib():
         "oq_codec_destroy": ([vp], None),
         "oq_compress": ([vp, vp, i32, sz, vp, vp], i32),
         "oq_compress_ex": ([vp, vp, i32, sz, vp, vp, vp], i32),
+        "oq_cache_append": ([vp, i32, vp, i32, C.c_uint64, vp, C.c_int64, vp, vp, C.c_uint64, vp],
+                            i32),
         "oq_decode": ([vp, vp, sz, vp, vp], i32),
         "oq_wire_header": ([cfgp, u64, C.c_char_p], i32),
         "oq_wire_parse_header": ([C.c_char_p, sz, cfgp, C.POINTER(u64)], i32),
@@ -392,6 +394,29 @@ class KVCache:
         _check(lib().oq_cache_pack(self.enc_v.handle, ROLE_V, _ptr(v_records), n, n_tokens, rs,
                                    _ptr(self.v), self.cap, _stream(stream)))
         self.tokens = n_tokens
+
+    def append(self, k, v, pos=None, stream=None):
+        """Decode step: compress one new key and value per stream (k, v: CUDA
+        [B, Hkv, dim]) and write them at token ``pos`` (an int, or a CUDA int64
+        tensor [B*Hkv] of per-stream positions; default: ``self.tokens``)."""
+        import torch
+        n = self.B * self.Hkv
+        p = self.tokens if pos is None else pos
+        L = lib()
+        for enc, x, tiles, role in ((self.enc_k, k, self.k, ROLE_K), (self.enc_v, v, self.v, ROLE_V)):
+            x = x.contiguous().reshape(n, enc.cfg.dim)
+            dt = _DTYPES.get(str(x.dtype).replace("torch.", ""))
+            if dt is None:
+                raise ValueError(f"unsupported dtype {x.dtype}")
+            recs = torch.empty((n, enc.record_bytes), dtype=torch.uint8, device=x.device)
+            if isinstance(p, int):
+                pd, ps = None, p
+            else:
+                pd, ps = _ptr(p.contiguous().to(torch.int64)), 0
+            _check(L.oq_cache_append(enc.handle, role, _ptr(x), dt, n, pd, ps, _ptr(recs),
+                                     _ptr(tiles), self.cap, _stream(stream)))
+        if isinstance(p, int):
+            self.tokens = max(self.tokens, p + 1)
 
     def nbytes_per_token(self):
         return (self.enc_k.tile_bytes(ROLE_K) + self.enc_v.tile_bytes(ROLE_V)) / 32.0

@@ -960,6 +960,86 @@ __global__ void pack_tiles_kernel(OqCodecParams p, int role, const uint8_t* __re
 }
 
 // ---------------------------------------------------------------------------
+// Decode-step append (oq_cache_append): write ONE token per stream — the
+// record rec[s] — into token slot pos of the stream's tile, leaving the other
+// 31 tokens of the tile untouched (read-modify-write of the W-bit fields in
+// the lane runs).  One warp per stream; only the lanes owning that token's
+// slots write.  Same bit layout as pack_tiles_kernel.
+__device__ __forceinline__ void put_field(uint32_t* codes, int W, int lane, int role, int slot,
+                                          uint32_t code) {
+  const int pos = slot * W, i = pos >> 5, sh = pos & 31;
+  auto word = [&](int wi) -> uint32_t& {
+    return codes[role == 0 ? k_word_off(W, lane, wi) : v_word_off(W, lane, wi)];
+  };
+  const uint32_t m = (1u << W) - 1u;
+  uint32_t& w0 = word(i);
+  w0 = (w0 & ~(m << sh)) | (code << sh);
+  if (sh + W > 32) {
+    uint32_t& w1 = word(i + 1);
+    const int hi = sh + W - 32;
+    w1 = (w1 & ~((1u << hi) - 1u)) | (code >> (W - hi));
+  }
+}
+
+__global__ void append_token_kernel(OqCodecParams p, int role, const uint8_t* __restrict__ recs,
+                                    size_t n_streams, const int64_t* __restrict__ pos_dev,
+                                    int64_t pos_scalar, uint8_t* __restrict__ tiles,
+                                    size_t tiles_cap) {
+  const int W = 2 * p.b_dir + p.b_nrm;
+  const int lane = threadIdx.x & 31;
+  const size_t s = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  if (s >= n_streams) return;
+  const int64_t pos = pos_dev ? pos_dev[s] : pos_scalar;
+  if (pos < 0 || (size_t)pos >= tiles_cap * 32) return;
+  const size_t tile = (size_t)pos / 32;
+  const int tt = (int)(pos % 32);
+  const int tb = role == 0 ? ktile_bytes(W, p.qjl) : vtile_bytes(W);
+  uint8_t* out = tiles + (s * tiles_cap + tile) * (size_t)tb;
+  const uint8_t* r = recs + s * p.rec_bytes;
+  const int g = lane >> 2, c = lane & 3;
+  const int tg = tt & 7, tk = tt >> 3;  // token = g + 8k in the K map and the gamma slots
+  if (lane == 0) {
+    const uint32_t b = (uint32_t)r[0] | ((uint32_t)r[1] << 8) | ((uint32_t)r[2] << 16) |
+                       ((uint32_t)r[3] << 24);
+    reinterpret_cast<float*>(out)[tg * 4 + tk] = __uint_as_float(b);
+  }
+  uint32_t* codes = reinterpret_cast<uint32_t*>(out + 128);
+  if (role == 0) {
+    if (g == tg) {
+      const int nu = c < 3 ? 11 : 10;
+      for (int u = 0; u < nu; ++u) put_field(codes, W, lane, 0, u * 4 + tk, rec_joint(p, r, 11 * c + u));
+      if (p.qjl) {
+        uint8_t* qa = out + 128 + 4 * kcode_words(W);
+        const int sign_off = 4 + p.dir_bytes + p.nrm_bytes + 2;
+        if (c == 0)
+          reinterpret_cast<uint16_t*>(qa)[tg * 4 + tk] =
+              (uint16_t)(r[sign_off - 2] | (r[sign_off - 1] << 8));
+        uint32_t w = 0;
+        for (int i = 0; i < 4; ++i) w |= (uint32_t)r[sign_off + 4 * c + i] << (8 * i);
+        reinterpret_cast<uint32_t*>(qa + 64)[(4 * g + c) * 4 + tk] = w;
+      }
+    }
+  } else {
+    // V map: token v_token(c, k) = 16 (k >> 2) + 2c + (k & 1) + 8 ((k >> 1) & 1)
+    if (c == ((tt & 7) >> 1)) {
+      const int k = (tt >> 4) * 4 + ((tt >> 3) & 1) * 2 + (tt & 1);
+      const int nu = g < 7 ? 6 : 1;
+      for (int u = 0; u < nu; ++u) put_field(codes, W, lane, 1, u * 8 + k, rec_joint(p, r, 6 * g + u));
+    }
+  }
+}
+
+cudaError_t launch_append_token(const OqCodecParams& p, int role, const uint8_t* recs,
+                                size_t n_streams, const int64_t* pos_dev, int64_t pos_scalar,
+                                uint8_t* tiles, size_t tiles_cap, cudaStream_t st) {
+  if (n_streams == 0) return cudaSuccess;
+  const size_t blocks = (n_streams * 32 + 255) / 256;
+  append_token_kernel<<<(unsigned)blocks, 256, 0, st>>>(p, role, recs, n_streams, pos_dev,
+                                                        pos_scalar, tiles, tiles_cap);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 size_t attention_tile_bytes(const OqCodecParams& p, int role) {
   const int W = 2 * p.b_dir + p.b_nrm;
   if (p.dim != 128 || W > 13 || W < 3) return 0;

@@ -455,6 +455,27 @@ oq_status oq_cache_pack(const oq_codec* c, int role, const void* records, uint64
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "pack tiles kernel");
 }
 
+oq_status oq_cache_append(const oq_codec* c, int role, const void* x, int dtype,
+                          uint64_t n_streams, const int64_t* pos_dev, int64_t pos, void* records,
+                          void* tiles, uint64_t cap_tokens, void* stream) {
+  oq_status s = check_codec(c);
+  if (s) return s;
+  if (role != OQ_ROLE_K && role != OQ_ROLE_V) return fail(OQ_ERR_INVALID_ARGUMENT, "bad role");
+  if (n_streams && (!x || !records || !tiles)) return fail(OQ_ERR_INVALID_ARGUMENT, "null buffer");
+  if (!pos_dev && (pos < 0 || (uint64_t)pos >= cap_tokens))
+    return fail(OQ_ERR_INVALID_ARGUMENT, "append position outside the cache");
+  if (oqd::attention_tile_bytes(c->p, role) == 0)
+    return fail(OQ_ERR_UNSUPPORTED, "attention tile format needs dim 128 and 2*b_dir+b_nrm <= 13");
+  if (role == OQ_ROLE_V && c->cfg.qjl)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "the V codec carries no QJL sidecar");
+  s = oq_compress(c, x, dtype, n_streams, records, stream);
+  if (s) return s;
+  cudaError_t e = oqd::launch_append_token(c->p, role, static_cast<const uint8_t*>(records),
+                                           n_streams, pos_dev, pos, static_cast<uint8_t*>(tiles),
+                                           (cap_tokens + 31) / 32, as_stream(stream));
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "append kernel");
+}
+
 static int parts_per_row(const oq_codec* ck, const oq_attn_shape* sh, uint64_t t0, uint64_t t1,
                          int n_splits) {
   return oqd::attention_num_parts(sh->B, sh->Hq, sh->Hkv, sh->T, t0, t1, n_splits, ck->num_sms);

@@ -60,6 +60,10 @@ bool attention_fast_path_ok(const OqCodecParams& pk, const OqCodecParams& pv);
 cudaError_t launch_pack_tiles(const OqCodecParams& p, int role, const uint8_t* recs,
                               size_t n_streams, size_t n_tokens, size_t rec_stride_tokens,
                               uint8_t* tiles, size_t tiles_cap, cudaStream_t st);
+// decode-step append: record recs[s] -> token slot pos (pos_dev[s] if set)
+cudaError_t launch_append_token(const OqCodecParams& p, int role, const uint8_t* recs,
+                                size_t n_streams, const int64_t* pos_dev, int64_t pos_scalar,
+                                uint8_t* tiles, size_t tiles_cap, cudaStream_t st);
 // K5: query prep -> mma fragments (a.qfrag)
 cudaError_t launch_qprep(const OqCodecParams& pk, const AttnArgs& a, cudaStream_t st);
 // K3: split-K partials over [t_begin, t_end)

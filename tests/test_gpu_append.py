@@ -1,0 +1,72 @@
+"""GPU: decode-step append path.
+
+oq_cache_append compresses one new key/value per (batch, kv head) stream and
+writes it into its token slot of the attention tiles.  Appending a sequence
+token by token must produce the very same tile bytes as compressing the whole
+sequence and packing it (oq_cache_pack), for K (with and without the QJL
+sidecar) and V, with uniform and per-stream (ragged) positions; attention
+over the appended cache then equals attention over the packed one.
+"""
+import numpy as np
+import pytest
+
+import paper_2605_21226_b200 as oq
+
+pytestmark = pytest.mark.gpu
+
+
+def _encoders(bits, qjl):
+    bd, bn = oq.default_bit_split(bits)
+    ek = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=21, qjl=qjl, qjl_seed=22))
+    ev = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=23))
+    return ek, ev
+
+
+@pytest.mark.parametrize("bits,qjl", [(3, False), (2, True), (2, False)])
+def test_append_equals_pack(cuda, bits, qjl):
+    import torch
+    B, Hkv, T, cap = 2, 2, 70, 96
+    n = B * Hkv
+    g = torch.Generator(device=cuda).manual_seed(7)
+    k = torch.randn((n, T, 128), device=cuda, generator=g)
+    v = torch.randn((n, T, 128), device=cuda, generator=g)
+    ek, ev = _encoders(bits, qjl)
+    packed = oq.KVCache(ek, ev, B, Hkv, cap)
+    kr = ek.compress(k.reshape(-1, 128)).reshape(n, T, -1)
+    vr = ev.compress(v.reshape(-1, 128)).reshape(n, T, -1)
+    packed.pack(kr, vr, T)
+    app = oq.KVCache(ek, ev, B, Hkv, cap)
+    for t in range(T):
+        app.append(k[:, t].reshape(B, Hkv, 128), v[:, t].reshape(B, Hkv, 128))
+    assert app.tokens == T
+    assert torch.equal(app.k, packed.k), "K tiles differ"
+    assert torch.equal(app.v, packed.v), "V tiles differ"
+    q = torch.randn((B, 7 * Hkv, 128), device=cuda, generator=g)
+    a = oq.attention_decode(q, app)
+    b = oq.attention_decode(q, packed)
+    assert torch.equal(a, b)
+
+
+def test_append_ragged_positions(cuda):
+    import torch
+    B, Hkv, cap = 3, 1, 96
+    ek, ev = _encoders(3, False)
+    lens = [5, 33, 40]
+    g = torch.Generator(device=cuda).manual_seed(9)
+    k = torch.randn((B, max(lens), 128), device=cuda, generator=g)
+    v = torch.randn((B, max(lens), 128), device=cuda, generator=g)
+    app = oq.KVCache(ek, ev, B, Hkv, cap)
+    # each step appends token t of every sequence still growing; finished ones
+    # are parked at position cap - 1 (a slot attention never reads here)
+    for t in range(max(lens)):
+        pos = torch.tensor([t if t < L else cap - 1 for L in lens], dtype=torch.int64, device=cuda)
+        app.append(k[:, t].reshape(B, 1, 128), v[:, t].reshape(B, 1, 128), pos=pos)
+    ref = oq.KVCache(ek, ev, B, Hkv, cap)
+    for b, L in enumerate(lens):
+        one = oq.KVCache(ek, ev, 1, 1, cap)
+        one.pack(ek.compress(k[b, :L]), ev.compress(v[b, :L]), L)
+        kt, vt = ek.tile_bytes(0), ev.tile_bytes(1)
+        ntile = (L + 31) // 32
+        per_k, per_v = (cap + 31) // 32 * kt, (cap + 31) // 32 * vt
+        assert torch.equal(app.k[b * per_k:b * per_k + ntile * kt], one.k[:ntile * kt]), b
+        assert torch.equal(app.v[b * per_v:b * per_v + ntile * vt], one.v[:ntile * vt]), b
