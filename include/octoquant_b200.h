@@ -30,7 +30,8 @@ typedef enum {
   OQ_ERR_INVALID_ARGUMENT = 1,
   OQ_ERR_FORMAT = 2,
   OQ_ERR_CUDA = 3,
-  OQ_ERR_UNSUPPORTED = 4
+  OQ_ERR_UNSUPPORTED = 4,
+  OQ_ERR_NCCL = 5
 } oq_status;
 
 /* Rounding (codec.hpp:34) */
@@ -167,6 +168,30 @@ oq_status oq_attention_partials(const oq_codec* ck, const oq_codec* cv,
 oq_status oq_attention_combine(const oq_codec* cv, const float* partials, int rows, int n_parts,
                                size_t row_stride, size_t part_stride, int finalize, float* out,
                                void* stream);
+
+/* ---- sequence-sharded decode attention over NCCL -------------
+ * This rank holds tokens [t_begin, t_end) of every stream in kcache/vcache
+ * (tile positions as in the full cache); `comm` is an ncclComm_t of nranks
+ * ranks.  The rank computes its partials (K5+K3), merges its splits (K4,
+ * finalize = 0), ONE ncclAllGather moves the [B*Hq][4 + dim] partials of all
+ * ranks, and every rank merges them in rank order — the chunk merge of
+ * attention_decode(..., n_splits = nranks) (attention.hpp:60-69) — so out
+ * [B, Hq, dim] is identical on all ranks.  NCCL (libnccl.so.2) is loaded on
+ * first use; OQ_ERR_NCCL if it is unavailable or a call fails. */
+size_t oq_attention_sharded_workspace_bytes(const oq_codec* ck, const oq_codec* cv,
+                                            const oq_attn_shape* shape, int n_splits,
+                                            int nranks);
+oq_status oq_attention_decode_sharded(const oq_codec* ck, const oq_codec* cv,
+                                      const oq_attn_shape* shape, const float* q,
+                                      const void* kcache, const void* vcache, uint64_t t_begin,
+                                      uint64_t t_end, void* nccl_comm, int nranks, float* out,
+                                      int n_splits, void* workspace, size_t ws_bytes,
+                                      void* stream);
+/* NCCL helpers for callers without their own NCCL setup (tests, the C++
+ * header): unique id (128 bytes) on one rank, broadcast it, then init. */
+oq_status oq_nccl_get_unique_id(uint8_t id[128]);
+oq_status oq_nccl_comm_init_rank(void** comm, int nranks, const uint8_t id[128], int rank);
+oq_status oq_nccl_comm_destroy(void* comm);
 
 /* ---- general path: any codec configuration, straight from OCTO records ----
  * Encoder::score(prepare(q), k) (codec.hpp:282-316): out[nq][n] fp32 for q

@@ -94,6 +94,12 @@ def lib():
         "oq_codec_destroy": ([vp], None),
         "oq_compress": ([vp, vp, i32, sz, vp, vp], i32),
         "oq_compress_ex": ([vp, vp, i32, sz, vp, vp, vp], i32),
+        "oq_attention_sharded_workspace_bytes": ([vp, vp, C.POINTER(_Shape), i32, i32], sz),
+        "oq_attention_decode_sharded": ([vp, vp, C.POINTER(_Shape), vp, vp, vp, C.c_uint64,
+                                         C.c_uint64, vp, i32, vp, i32, vp, sz, vp], i32),
+        "oq_nccl_get_unique_id": ([vp], i32),
+        "oq_nccl_comm_init_rank": ([C.POINTER(vp), i32, vp, i32], i32),
+        "oq_nccl_comm_destroy": ([vp], i32),
         "oq_cache_append": ([vp, i32, vp, i32, C.c_uint64, vp, C.c_int64, vp, vp, C.c_uint64, vp],
                             i32),
         "oq_decode": ([vp, vp, sz, vp, vp], i32),
@@ -539,6 +545,53 @@ def attention_partials(q, cache: KVCache, t_begin, t_end, n_splits=None, T=None,
     _check(L.oq_attention_partials(cache.enc_k.handle, cache.enc_v.handle, C.byref(sh), _ptr(q),
                                    _ptr(cache.k), _ptr(cache.v), t_begin, t_end, _ptr(out),
                                    n_splits, _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
+class NcclComm:
+    """An NCCL communicator created through the library's own NCCL loader
+    (libnccl.so.2): ``uid = NcclComm.unique_id()`` on one rank, share it, then
+    ``NcclComm(nranks, uid, rank)`` on every rank (one GPU each)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(lib().oq_nccl_get_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, nranks: int, uid: bytes, rank: int):
+        self.nranks, self.rank = nranks, rank
+        self.handle = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().oq_nccl_comm_init_rank(C.byref(self.handle), nranks, buf, rank))
+
+    def close(self):
+        if self.handle:
+            _check(lib().oq_nccl_comm_destroy(self.handle))
+            self.handle = C.c_void_p()
+
+
+def attention_decode_sharded(q, cache: KVCache, t_begin, t_end, comm: NcclComm, n_splits=None,
+                             T=None, out=None, stream=None):
+    """Sequence-sharded attention_decode: this rank's tokens [t_begin, t_end),
+    one NCCL all-gather of the partials, rank-ordered merge (identical output
+    on every rank)."""
+    import torch
+    B, Hq, D = q.shape
+    T = cache.tokens if T is None else T
+    n_splits = 0 if n_splits is None else n_splits
+    sh = _shape(cache, Hq, T, None)
+    L = lib()
+    ws_bytes = L.oq_attention_sharded_workspace_bytes(cache.enc_k.handle, cache.enc_v.handle,
+                                                      C.byref(sh), n_splits, comm.nranks)
+    ws = _Workspace.get(ws_bytes, q.device)
+    if out is None:
+        out = torch.empty((B, Hq, D), dtype=torch.float32, device=q.device)
+    q = q.contiguous().float()
+    _check(L.oq_attention_decode_sharded(cache.enc_k.handle, cache.enc_v.handle, C.byref(sh),
+                                         _ptr(q), _ptr(cache.k), _ptr(cache.v), t_begin, t_end,
+                                         comm.handle, comm.nranks, _ptr(out), n_splits, _ptr(ws),
+                                         ws.numel(), _stream(stream)))
     return out
 
 

@@ -4,6 +4,7 @@
 // data-path entry point launches an sm_100a kernel.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <cmath>
 #include <cstring>
@@ -583,6 +584,51 @@ oq_status oq_attention_decode(const oq_codec* ck, const oq_codec* cv, const oq_a
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "combine kernel");
 }
 
+// ---- NCCL, loaded on first use (no link-time dependency) -------------------
+namespace {
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  // signatures from nccl.h (ncclResult_t is an int enum; ncclFloat32 = 7)
+  int (*all_gather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*user_rank)(void*, int*) = nullptr;
+  int (*count)(void*, int*) = nullptr;
+  int (*get_unique_id)(void*) = nullptr;
+  int (*init_rank)(void**, int, const void*, int) = nullptr;  // id passed by value (128 B)
+  int (*destroy)(void*) = nullptr;
+  const char* (*err)(int) = nullptr;
+};
+struct NcclUid {
+  char b[128];
+};
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = "libnccl.so.2 not found";
+      return a;
+    }
+    a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+    a.user_rank = reinterpret_cast<decltype(a.user_rank)>(dlsym(h, "ncclCommUserRank"));
+    a.count = reinterpret_cast<decltype(a.count)>(dlsym(h, "ncclCommCount"));
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.init_rank = reinterpret_cast<decltype(a.init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.err = reinterpret_cast<decltype(a.err)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.all_gather && a.user_rank && a.count && a.get_unique_id && a.init_rank &&
+           a.destroy && a.err;
+    if (!a.ok) a.why = "libnccl lacks the expected symbols";
+    return a;
+  }();
+  return api;
+}
+oq_status nccl_fail(int r, const char* what) {
+  return fail(OQ_ERR_NCCL, std::string(what) + ": " + (nccl().err ? nccl().err(r) : "error"));
+}
+}  // namespace
+
 oq_status oq_attention_partials(const oq_codec* ck, const oq_codec* cv, const oq_attn_shape* sh,
                                 const float* q, const void* kc, const void* vc, uint64_t t0,
                                 uint64_t t1, float* partial, int n_splits, void* ws,
@@ -612,6 +658,79 @@ oq_status oq_attention_combine(const oq_codec* cv, const float* partials, int ro
   cudaError_t e = oqd::launch_attention_combine(cv->p, partials, rows, n_parts, row_stride,
                                                 part_stride, finalize, out, as_stream(stream));
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "combine kernel");
+}
+
+size_t oq_attention_sharded_workspace_bytes(const oq_codec* ck, const oq_codec* cv,
+                                            const oq_attn_shape* sh, int n_splits, int nranks) {
+  const size_t base = oq_attention_workspace_bytes(ck, cv, sh, n_splits);
+  if (!base || nranks < 1) return 0;
+  const size_t gather = (size_t)nranks * sh->B * sh->Hq * (4 + ck->cfg.dim) * sizeof(float);
+  return ((base + 255) & ~size_t(255)) + gather;
+}
+
+oq_status oq_attention_decode_sharded(const oq_codec* ck, const oq_codec* cv,
+                                      const oq_attn_shape* sh, const float* q, const void* kc,
+                                      const void* vc, uint64_t t0, uint64_t t1, void* comm,
+                                      int nranks, float* out, int n_splits, void* ws,
+                                      size_t ws_bytes, void* stream) {
+  const size_t base = oq_attention_workspace_bytes(ck, cv, sh, n_splits);
+  oq_status s = attn_check(ck, cv, sh, q, kc, vc, n_splits, base);
+  if (s) return s;
+  if (!out || !ws || !comm || nranks < 1) return fail(OQ_ERR_INVALID_ARGUMENT, "null argument");
+  if (t0 > t1 || t1 > sh->T) return fail(OQ_ERR_INVALID_ARGUMENT, "bad token range");
+  if (ws_bytes < oq_attention_sharded_workspace_bytes(ck, cv, sh, n_splits, nranks))
+    return fail(OQ_ERR_INVALID_ARGUMENT, "workspace too small");
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(OQ_ERR_NCCL, api.why);
+  int rank = -1, count = 0, r;
+  if ((r = api.user_rank(comm, &rank)) != 0) return nccl_fail(r, "ncclCommUserRank");
+  if ((r = api.count(comm, &count)) != 0) return nccl_fail(r, "ncclCommCount");
+  if (count != nranks) return fail(OQ_ERR_INVALID_ARGUMENT, "nranks differs from the communicator");
+  const cudaStream_t st = as_stream(stream);
+  const int rows = sh->B * sh->Hq;
+  const size_t w = 4 + ck->cfg.dim, per = (size_t)rows * w;
+  float* gather = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + ((base + 255) & ~size_t(255)));
+  float* parts = nullptr;
+  int np = 0;
+  s = run_partials(ck, cv, sh, q, kc, vc, t0, t1, n_splits, ws, st, &parts, &np);
+  if (s) return s;
+  // merge this rank's splits straight into its slot of the gather buffer
+  cudaError_t e = oqd::launch_attention_combine(cv->p, parts, rows, np, np * w, w, 0,
+                                                gather + (size_t)rank * per, st);
+  if (e != cudaSuccess) return cuda_fail(e, "combine kernel");
+  // the only collective: in-place all-gather of the per-rank partials
+  if ((r = api.all_gather(gather + (size_t)rank * per, gather, per, /*ncclFloat32*/ 7, comm, st)) != 0)
+    return nccl_fail(r, "ncclAllGather");
+  e = oqd::launch_attention_combine(cv->p, gather, rows, nranks, w, per, 1, out, st);
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "combine kernel");
+}
+
+oq_status oq_nccl_get_unique_id(uint8_t id[128]) {
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(OQ_ERR_NCCL, api.why);
+  if (!id) return fail(OQ_ERR_INVALID_ARGUMENT, "null id");
+  const int r = api.get_unique_id(id);
+  return r ? nccl_fail(r, "ncclGetUniqueId") : OQ_OK;
+}
+
+oq_status oq_nccl_comm_init_rank(void** comm, int nranks, const uint8_t id[128], int rank) {
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(OQ_ERR_NCCL, api.why);
+  if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "bad communicator arguments");
+  // ncclCommInitRank takes the 128-byte unique id by value
+  using InitFn = int (*)(void**, int, NcclUid, int);
+  NcclUid u;
+  std::memcpy(u.b, id, 128);
+  const int r = reinterpret_cast<InitFn>(api.init_rank)(comm, nranks, u, rank);
+  return r ? nccl_fail(r, "ncclCommInitRank") : OQ_OK;
+}
+
+oq_status oq_nccl_comm_destroy(void* comm) {
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(OQ_ERR_NCCL, api.why);
+  const int r = comm ? api.destroy(comm) : 0;
+  return r ? nccl_fail(r, "ncclCommDestroy") : OQ_OK;
 }
 
 oq_status oq_scores(const oq_codec* c, const float* q, int nq, const void* records, size_t n,
