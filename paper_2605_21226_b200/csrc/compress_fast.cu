@@ -11,9 +11,12 @@
 //    and stored as float(gamma) (codec.hpp:219-233);
 //  * the rotation runs in fp32 registers (signs, 7-stage WHT, one scale by
 //    float(inv / sqrt(d))).  Its error against the reference's fp64 rotated
-//    coordinates is bounded: |ur32 - ur64| <= E0 = 9.1 u (u = 2^-24; 7 u
-//    ||k||_1 / (gamma sqrt d) <= 7 u from the butterflies, 2 u from the
-//    scale, |ur| <= 1), see DESIGN.md §2;
+//    coordinates is bounded in L2 over the whole vector: each of the 7
+//    butterfly stages adds <= u |v_s| (u = 2^-24), |v_s| = 2^((s+1)/2) |k|,
+//    and the later stages grow it by 2^((6-s)/2), so after the scale by
+//    1/(gamma sqrt d) the butterflies contribute <= 7u, the scale <= 2u per
+//    coordinate: for a triplet ||t32 - t64|| <= Et = 7.01u + 2.01u ||t||
+//    (see DESIGN.md §2);
 //  * every decision of the triplet encoder — octahedral hemisphere and
 //    signs (octahedral.hpp:22-31), the xi/eta bucket (lloydmax.hpp:46-49),
 //    the 3x3 argmax (codec.hpp:164-189) and the norm bucket — is taken in
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(kCFThreads, 1)
   using S = CFS<BD, BN>;
   constexpr int K = S::K;
   constexpr float U = 5.9604645e-8f;  // 2^-24
-  constexpr float E0 = 9.1f * U;      // |ur32 - ur64| bound (see the header)
+  constexpr float E0 = 7.02f * U;     // triplet-independent part of Et (see the header)
   extern __shared__ __align__(128) uint8_t smem[];
   float4* dirs = reinterpret_cast<float4*>(smem);
   float4* lut = reinterpret_cast<float4*>(smem + S::DIRS_BYTES);
@@ -250,11 +253,15 @@ __global__ void __launch_bounds__(kCFThreads, 1)
         const float l1 = a0 + a1 + a2;
         float il;  // rcp.approx: relative error <= 2^-23
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(il) : "f"(l1));
-        // |d xi| <= (|dt0| + |xi| |dl1|) / l1 + rounding <= 4 E0 / l1 + 5u
-        const float gx = 4.f * E0 * il * 1.001f + 6.f * U;
+        // Et = E0 + 2.01u |t| <= E0 + 2.01u l1.  xi = t0 / l1 (or 1 - |t1| / l1):
+        // |d xi| <= (|dt0| + |xi| |dl1|) / l1 <= (1 + sqrt 3) Et / l1, plus <= 8u
+        // of fp32 rounding and u for the fp32 boundaries
+        const float gx = (2.74f * E0 * il + 5.51f * U + 9.f * U) * 1.001f;
         const bool up = pad || t2 >= 0.f;  // octahedral.hpp:28 (pad: pz = 0 exactly)
-        // hemisphere and, below it, sgn(px), sgn(py) (octahedral.hpp:29-30)
-        ok = ok && l1 > 1e-6f && (pad || a2 > E0) && (up || (a0 > E0 && a1 > E0));
+        // hemisphere and, below it, sgn(px), sgn(py) (octahedral.hpp:29-30):
+        // |t_i| > E0 + 2.01u |t_i| is implied by |t_i| > 1.0001 E0
+        const float es = 1.0001f * E0;
+        ok = ok && l1 > 1e-6f && (pad || a2 > es) && (up || (a0 > es && a1 > es));
         const float xi = up ? t0 * il : copysignf(1.f - a1 * il, t0);
         const float eta = up ? t1 * il : copysignf(1.f - a0 * il, t1);
         const uint32_t sx = cf_bucket(xi, gx, mylut, ok);
@@ -263,7 +270,7 @@ __global__ void __launch_bounds__(kCFThreads, 1)
         float rv, gr;
         if (MODE == 0) {  // scalar: rho of clamp(|t|, 0, 1) (codec.hpp:154-162)
           rv = sqrtf(fmaf(t2, t2, fmaf(t1, t1, t0 * t0)));
-          gr = 1.7321f * E0 + 4.f * U;
+          gr = (E0 + 4.6f * U * l1) * 1.001f;  // Et + fp32 sum/sqrt rounding
         } else {  // local3x3 (codec.hpp:164-192): strict '>' argmax over the window
           float b1 = -INFINITY, b2 = -INFINITY;
           uint32_t wi = 0;
@@ -280,9 +287,10 @@ __global__ void __launch_bounds__(kCFThreads, 1)
               b1 = fmaxf(b1, sc);
               wi = gt ? (uint32_t)(da * 4 + db) : wi;
             }
-          // score error: sqrt(3) E0 (rotation) + sqrt(3) u (fp32 table) + 3u (dot)
-          const float gs = 1.7321f * E0 + 5.f * U;
-          ok = ok && (b1 - b2 > 2.f * gs);
+          // score error: ||dt|| <= Et (rotation) + |t| u/2 (fp32 table) + 3u |t|
+          // (dot rounding), with |t| <= l1
+          const float gs = (E0 + 5.53f * U * l1) * 1.001f;
+          ok = ok && (b1 - b2 > 2.002f * gs);
           ix = sx + (wi >> 2) - 1;
           iy = sy + (wi & 3) - 1;
           rv = b1;
