@@ -420,22 +420,22 @@ def main():
     return 0
 
 
-def bench_compress(oq, torch, dev, bits, world, barrier, dist, peak):
-    """K1 at BASELINE configs[1]: 2^20 fp32 keys -> OCTO records, bit-exact."""
-    n = 1 << 20
+def _codec_times(oq, torch, dev, bits, x, world, dist, steps=10):
+    """K1 and K2 over x ([n, 128] fp32) at `bits`: mean device ms per call (max over
+    ranks), records bytes, flagged-key count of the certified pass."""
+    n = x.shape[0]
     bd, bn = oq.default_bit_split(bits)
     enc = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn))
-    x = torch.randn((n, 128), device=dev, generator=torch.Generator(device=dev).manual_seed(5))
     recs = torch.empty((n, enc.record_bytes), dtype=torch.uint8, device=dev)
     dec = torch.empty((n, 128), dtype=torch.float32, device=dev)
+    fl = torch.zeros(1, dtype=torch.int32, device=dev)
     for _ in range(3):
-        enc.compress(x, out=recs)
+        enc.compress(x, out=recs, flagged=fl)
         enc.decode(recs, out=dec)
     torch.cuda.synchronize()
-    steps = 10
     oq.timing(True)
     for _ in range(steps):
-        enc.compress(x, out=recs)
+        enc.compress(x, out=recs, flagged=fl)
         enc.decode(recs, out=dec)
     c_ms, c_n = oq.timing_collect("compress")
     d_ms, d_n = oq.timing_collect("decode")
@@ -444,15 +444,39 @@ def bench_compress(oq, torch, dev, bits, world, barrier, dist, peak):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     cm, dm = (float(v) for v in t.tolist())
-    nbytes = n * (512 + enc.record_bytes)
-    return {"metric": "compress tokens/s", "value": world * n / (cm * 1e-3), "unit": "tokens/s",
+    return cm, dm, enc.record_bytes, int(fl.item())
+
+
+def bench_compress(oq, torch, dev, bits, world, barrier, dist, peak):
+    """K1 + K2 at BASELINE configs[1]: 2^20 fp32 keys -> OCTO records (bit-exact with
+    the reference, see tests/test_gpu_codec.py) and back, for b in {2, 3, 4}; the
+    top-level numbers are the headline bit width."""
+    n = 1 << 20
+    x = torch.randn((n, 128), device=dev, generator=torch.Generator(device=dev).manual_seed(5))
+    sweep = {}
+    for b in (2, 3, 4):
+        cm, dm, rb, flagged = _codec_times(oq, torch, dev, b, x, world, dist)
+        nbytes = n * (512 + rb)
+        sweep[str(b)] = {
+            "compress_ms": cm, "compress_keys_per_s": world * n / (cm * 1e-3),
+            "compress_gbs": nbytes / (cm * 1e-3) / 1e9,
+            "compress_frac_of_hbm": nbytes / (cm * 1e-3) / 1e9 / peak,
+            "flagged_keys": flagged,
+            "decode_ms": dm, "decode_keys_per_s": world * n / (dm * 1e-3),
+            "decode_gbs": nbytes / (dm * 1e-3) / 1e9,
+            "decode_frac_of_hbm": nbytes / (dm * 1e-3) / 1e9 / peak,
+            "bytes_per_key": 512 + rb}
+    h = sweep[str(bits)]
+    return {"metric": "compress tokens/s", "value": h["compress_keys_per_s"], "unit": "tokens/s",
             "config": {"workload": "C2: 2^20 keys d=128 fp32 in, local3x3, OCTO records out",
                        "bits": bits},
-            "ms": cm, "gbs": nbytes / (cm * 1e-3) / 1e9, "frac_of_hbm": nbytes / (cm * 1e-3) / 1e9
-            / peak,
-            "decode": {"metric": "decode tokens/s", "value": world * n / (dm * 1e-3), "ms": dm,
-                       "gbs": nbytes / (dm * 1e-3) / 1e9,
-                       "frac_of_hbm": nbytes / (dm * 1e-3) / 1e9 / peak}}
+            "ms": h["compress_ms"], "gbs": h["compress_gbs"], "frac_of_hbm": h["compress_frac_of_hbm"],
+            "traffic": ncu_traffic("compress_fast_kernel<4, 2, 2>"),
+            "decode": {"metric": "decode tokens/s", "value": h["decode_keys_per_s"],
+                       "ms": h["decode_ms"], "gbs": h["decode_gbs"],
+                       "frac_of_hbm": h["decode_frac_of_hbm"],
+                       "traffic": ncu_traffic("decode128_kernel<4, 2>")},
+            "sweep_bits": sweep}
 
 
 if __name__ == "__main__":

@@ -233,7 +233,6 @@ __global__ void __launch_bounds__(256) decode_kernel(OqCodecParams p,
 // segments.  Shared traffic per key: record staging, 43 direction + 43 norm
 // lookups and the output transpose.
 constexpr int kD128Threads = 128;            // 4 warps, 128 keys per block
-constexpr int kD128Rep = 8;                  // direction-table replicas (lane & 7)
 constexpr int kD128HalfStride = 68;          // floats per staged half row (64 + 4)
 
 template <int BD, int BN>
@@ -243,6 +242,10 @@ struct D128 {
   static constexpr int BYTES = 4 + DIRB + NRMB;           // without the QJL sidecar
   static constexpr int WORDS = (BYTES + 3) / 4;           // aligned record words used
   static constexpr int NPAIR = 1 << (2 * BD), NRHO = 1 << BN;
+  // direction-table replicas (lane & (REP - 1)): 8 keep the 8-lane phases of
+  // LDS.128 conflict-free; at b_dir = 5 (1024 directions) 2 keep the table at
+  // 32 KB so three CTAs still fit per SM
+  static constexpr int REP = BD <= 4 ? 8 : 2;
 };
 
 // `bits` (<= 16) at static bit position `pos` of the thread's record words.
@@ -286,8 +289,8 @@ __global__ void __launch_bounds__(kD128Threads, 3) decode128_kernel(OqCodecParam
                                                                  int aligned) {
   using S = D128<BD, BN>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  float4* dirs_s = reinterpret_cast<float4*>(smem_raw);                // [NPAIR][kD128Rep]
-  float* rho_s = reinterpret_cast<float*>(dirs_s + S::NPAIR * kD128Rep);  // [NRHO]
+  float4* dirs_s = reinterpret_cast<float4*>(smem_raw);                // [NPAIR][S::REP]
+  float* rho_s = reinterpret_cast<float*>(dirs_s + S::NPAIR * S::REP);  // [NRHO]
   float* half_s = rho_s + 16;                                           // [4 warps][32][68]
   uint64_t* bars = reinterpret_cast<uint64_t*>(half_s + 4 * 32 * kD128HalfStride);  // [2]
   uint8_t* stage0 = reinterpret_cast<uint8_t*>(bars + 2);  // 2 x [128 records], 16-aligned
@@ -296,12 +299,12 @@ __global__ void __launch_bounds__(kD128Threads, 3) decode128_kernel(OqCodecParam
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // direction table in field-pair order pr = ixi | ieta << b_dir
-  for (int i = tid; i < S::NPAIR * kD128Rep; i += kD128Threads) {
-    const int pr = i / kD128Rep, a = pr & ((1 << BD) - 1), b = pr >> BD;
+  for (int i = tid; i < S::NPAIR * S::REP; i += kD128Threads) {
+    const int pr = i / S::REP, a = pr & ((1 << BD) - 1), b = pr >> BD;
     dirs_s[i] = reinterpret_cast<const float4*>(p.dirs32)[(a << BD) | b];
   }
   for (int i = tid; i < S::NRHO; i += kD128Threads) rho_s[i] = p.rho32[i];
-  const float4* dtab = dirs_s + (lane & (kD128Rep - 1));
+  const float4* dtab = dirs_s + (lane & (S::REP - 1));
   float* hs = half_s + warp * 32 * kD128HalfStride;
   const float isd = (float)p.inv_sqrt_d;
   const size_t nblk = (n + kD128Threads - 1) / kD128Threads;
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(kD128Threads, 3) decode128_kernel(OqCodecParam
       for (int t = 0; t < S::NT; ++t) {
         const uint32_t pr = recfield(w, 32 + 2 * BD * t, 2 * BD);
         const uint32_t ir = recfield(w, 32 + 8 * S::DIRB + BN * t, BN);
-        const float4 d4 = dtab[pr * kD128Rep];
+        const float4 d4 = dtab[pr * S::REP];
         const float r = rho_s[ir];
         y[3 * t] = r * d4.x;  // reconstruct_rotated, codec.hpp:252-266
         if (3 * t + 1 < 128) y[3 * t + 1] = r * d4.y;
@@ -413,7 +416,7 @@ template <int BD, int BN>
 static cudaError_t launch_decode128(const OqCodecParams& p, const uint8_t* recs, size_t n,
                                    float* out, cudaStream_t st, int num_sms) {
   using S = D128<BD, BN>;
-  const size_t smem = (size_t)S::NPAIR * kD128Rep * 16 + 16 * 4 + 4 * 32 * kD128HalfStride * 4 +
+  const size_t smem = (size_t)S::NPAIR * S::REP * 16 + 16 * 4 + 4 * 32 * kD128HalfStride * 4 +
                       16 + 2 * (((size_t)kD128Threads * p.rec_bytes + 15) & ~size_t(15)) + 64;
   cudaError_t e = cudaFuncSetAttribute(decode128_kernel<BD, BN>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

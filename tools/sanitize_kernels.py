@@ -1,0 +1,29 @@
+"""Small invocation of every hot kernel (for compute-sanitizer runs)."""
+import os, sys
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+import torch
+import paper_2605_21226_b200 as oq
+
+dev = torch.device("cuda:0")
+g = torch.Generator(device=dev).manual_seed(1)
+for bits in (2, 3, 4):
+    for rnd in ("local3x3", "scalar"):
+        bd, bn = oq.default_bit_split(bits)
+        enc = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rounding=rnd))
+        x = torch.randn((3000, 128), device=dev, generator=g)   # partial tail blocks too
+        r = enc.compress(x)
+        enc.decode(r)
+B, Hkv, T = 2, 2, 300
+bd, bn = oq.default_bit_split(3)
+ek = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=5))
+ev = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=6))
+k = torch.randn((B * Hkv * T, 128), device=dev, generator=g)
+v = torch.randn((B * Hkv * T, 128), device=dev, generator=g)
+cache = oq.KVCache(ek, ev, B, Hkv, T + 40)
+cache.pack(ek.compress(k), ev.compress(v), T)
+cache.append(torch.randn((B, Hkv, 128), device=dev), torch.randn((B, Hkv, 128), device=dev))
+q = torch.randn((B, 7 * Hkv, 128), device=dev, generator=g)
+oq.attention_decode(q, cache)
+oq.attention_partials(q, cache, 0, cache.tokens)
+torch.cuda.synchronize()
+print("sanitize run ok")
