@@ -460,9 +460,12 @@ class _Workspace:
     buf = {}
 
     @classmethod
-    def get(cls, nbytes, device):
+    def get(cls, nbytes, device, kind="tile"):
+        """kind "tile": the compressed-cache attention workspace (its first
+        64 KiB are arrival counters that must stay zero between calls, so it is
+        never shared with other scratch uses); "dense": the general path."""
         import torch
-        key = str(device)
+        key = (str(device), kind)
         b = cls.buf.get(key)
         if b is None or b.numel() < nbytes:
             # zeroed once: the attention kernels keep their arrival counters
@@ -518,7 +521,7 @@ def attention_decode_dense(enc: Encoder, q, records, values, n_splits=1, stream=
         raise ValueError("values/cache length mismatch")
     L = lib()
     ws_bytes = L.oq_attention_dense_workspace_bytes(nq, max(1, n_splits), vdim)
-    ws = _Workspace.get(ws_bytes, q.device)
+    ws = _Workspace.get(ws_bytes, q.device, kind="dense")
     out = torch.empty((nq, vdim), dtype=torch.float32, device=q.device)
     _check(L.oq_attention_decode_dense(enc.handle, _ptr(q), nq, _ptr(records), n, _ptr(values),
                                        vdim, n_splits, _ptr(out), _ptr(ws), ws.numel(),

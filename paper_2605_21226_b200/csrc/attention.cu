@@ -245,6 +245,20 @@ struct TileRegs {
   uint4 sg;
 };
 
+// Streamed once: no L1 allocation for the tile data (it never hits again).
+__device__ __forceinline__ uint32_t ldg_na(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 ldg_na(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
 template <int W, bool QJL>
 __device__ __forceinline__ void load_tile(TileRegs<W, QJL>& r, const AttnKParams& P,
                                           size_t stream, size_t tile, int g, int c, int kl,
@@ -254,18 +268,18 @@ __device__ __forceinline__ void load_tile(TileRegs<W, QJL>& r, const AttnKParams
   using C = Cfg<W, QJL>;
   const uint8_t* kt = P.kcache + (stream * P.k_tiles_cap + tile) * (size_t)C::KTILE;
   const uint8_t* vt = P.vcache + (stream * P.v_tiles_cap + tile) * (size_t)C::VTILE;
-  r.gk = __ldg(reinterpret_cast<const float4*>(kt) + g);
-  r.gv = __ldg(reinterpret_cast<const float4*>(vt) + g);
+  r.gk = ldg_na(reinterpret_cast<const float4*>(kt) + g);
+  r.gv = ldg_na(reinterpret_cast<const float4*>(vt) + g);
   const uint32_t* kw = reinterpret_cast<const uint32_t*>(kt + 128);
   const uint32_t* vw = reinterpret_cast<const uint32_t*>(vt + 128);
 #pragma unroll
   for (int i = 0; i < C::KWF; ++i)
-    r.kc[i] = i < C::KW3 ? __ldg(kw + 32 * i + kl)
-                         : (c < 3 ? __ldg(kw + 32 * C::KW3 + 24 * (i - C::KW3) + 3 * g + c) : 0u);
+    r.kc[i] = i < C::KW3 ? ldg_na(kw + 32 * i + kl)
+                         : (c < 3 ? ldg_na(kw + 32 * C::KW3 + 24 * (i - C::KW3) + 3 * g + c) : 0u);
 #pragma unroll
   for (int i = 0; i < C::VWF; ++i)
-    r.vc[i] = i < C::VW7 ? __ldg(vw + 32 * i + vl)
-                         : (g < 7 ? __ldg(vw + 32 * C::VW7 + 28 * (i - C::VW7) + vl) : 0u);
+    r.vc[i] = i < C::VW7 ? ldg_na(vw + 32 * i + vl)
+                         : (g < 7 ? ldg_na(vw + 32 * C::VW7 + 28 * (i - C::VW7) + vl) : 0u);
   if (QJL) {
     const uint8_t* qa = kt + 128 + 4 * C::KCODE;
     r.gr = __ldg(reinterpret_cast<const uint2*>(qa) + g);
