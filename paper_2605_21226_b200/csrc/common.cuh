@@ -73,6 +73,43 @@ __device__ __forceinline__ double load_as_double(const void* p, int dtype, size_
   }
 }
 
+// Element size and exact fp32 widening of the input types the fast K1
+// kernels accept (fp32, fp16, bf16); 16-bit elements are in the low half.
+template <int DT>
+struct InElem {
+  static constexpr int BYTES = DT == OQ_F32 ? 4 : 2;
+};
+template <int DT>
+__device__ __forceinline__ float widen16(uint32_t b) {
+  if (DT == OQ_BF16) return __uint_as_float(b << 16);
+  return __half2float(__ushort_as_half((unsigned short)b));
+}
+// N consecutive elements of a 16-byte-aligned shared row -> fp32 registers.
+template <int DT, int N>
+__device__ __forceinline__ void load_elems(float (&y)[N], const void* row, int first = 0) {
+  if constexpr (DT == OQ_F32) {
+#pragma unroll
+    for (int i = 0; i < N / 4; ++i) {
+      const float4 v = reinterpret_cast<const float4*>(row)[i];
+      y[first + 4 * i] = v.x;
+      y[first + 4 * i + 1] = v.y;
+      y[first + 4 * i + 2] = v.z;
+      y[first + 4 * i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N / 8; ++i) {
+      const uint4 v = reinterpret_cast<const uint4*>(row)[i];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        y[first + 8 * i + 2 * j] = widen16<DT>(w[j] & 0xffffu);
+        y[first + 8 * i + 2 * j + 1] = widen16<DT>(w[j] >> 16);
+      }
+    }
+  }
+}
+
 // Read `bits` (<= 24) starting at bit `pos` of an LSB-first byte stream.
 __device__ __forceinline__ uint32_t read_bits(const uint8_t* s, uint32_t pos, uint32_t bits) {
   const uint32_t byte = pos >> 3, sh = pos & 7;

@@ -516,7 +516,7 @@ cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, si
   if (impl == 0 && compress_fast_ok(p, dtype, x, out)) {
     cudaError_t e = flagged ? cudaMemsetAsync(flagged, 0, sizeof(uint32_t), st) : cudaSuccess;
     if (e == cudaSuccess)
-      e = launch_compress_x2(p, static_cast<const float*>(x), n, out, st, num_sms);
+      e = launch_compress_x2(p, x, dtype, n, out, st, num_sms);
     return e;
   }
   if (impl == 1 && compress_fast_ok(p, dtype, x, out)) {
@@ -527,9 +527,9 @@ cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, si
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(ws, 0, sizeof(uint32_t), st);
     if (e == cudaSuccess)
-      e = launch_compress_fast(p, static_cast<const float*>(x), n, out, ws + 4, ws, st, num_sms);
+      e = launch_compress_fast(p, x, dtype, n, out, ws + 4, ws, st, num_sms);
     if (e == cudaSuccess)
-      e = launch_compress_x2(p, static_cast<const float*>(x), n, out, st, num_sms, ws + 4, ws);
+      e = launch_compress_x2(p, x, dtype, n, out, st, num_sms, ws + 4, ws);
     if (e == cudaSuccess && flagged)
       e = cudaMemcpyAsync(flagged, ws, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
     const cudaError_t f = cudaFreeAsync(ws, st);

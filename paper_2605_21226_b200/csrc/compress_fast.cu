@@ -1,5 +1,5 @@
 // compress_fast.cu — K1 fast path: Encoder::encode (codec.hpp:214-249) for
-// d = 128, fp32 keys, scalar / local3x3 rounding, no QJL, at the BASELINE bit
+// d = 128, fp32 / fp16 / bf16 keys, scalar / local3x3 rounding, no QJL, at the BASELINE bit
 // splits (3,1), (4,2), (5,3).  ONE KEY PER THREAD, certified fp32:
 //
 //  * each warp owns 32 consecutive keys; every lane pulls its 512-byte row
@@ -81,9 +81,9 @@ __device__ __forceinline__ uint32_t cf_bucket(float x, float g, const float4* lu
   return (uint32_t)lo + (upx ? 1u : 0u);
 }
 
-template <int BD, int BN, int MODE>
+template <int BD, int BN, int MODE, int DT>
 __global__ void __launch_bounds__(kCFThreads, 1)
-    compress_fast_kernel(OqCodecParams p, const float* __restrict__ x, size_t n,
+    compress_fast_kernel(OqCodecParams p, const void* __restrict__ x, size_t n,
                          uint8_t* __restrict__ out, uint32_t* __restrict__ flag_idx,
                          uint32_t* __restrict__ flag_cnt) {
   using S = CFS<BD, BN>;
@@ -149,16 +149,18 @@ __global__ void __launch_bounds__(kCFThreads, 1)
   auto request = [&](size_t blk) {  // rows of block blk -> this warp's staging rows
     const size_t k0 = blk * 32;
     const int nk = (int)min((size_t)32, n - k0);
+    constexpr int RB_IN = 128 * InElem<DT>::BYTES;  // bytes per input row
     if (lane == 0)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cf_smem(bar)),
-                   "r"(nk * 512)
+                   "r"(nk * RB_IN)
                    : "memory");
     __syncwarp();
     if (lane < nk)
       asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, "
-          "[%2];" ::"r"(cf_smem(myrow)),
-          "l"(x + (k0 + lane) * 128), "r"(cf_smem(bar))
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+          "[%3];" ::"r"(cf_smem(myrow)),
+          "l"(static_cast<const uint8_t*>(x) + (k0 + lane) * RB_IN), "n"(RB_IN),
+          "r"(cf_smem(bar))
           : "memory");
   };
   size_t blk = (size_t)blockIdx.x * kCFWarps + warp;
@@ -173,14 +175,7 @@ __global__ void __launch_bounds__(kCFThreads, 1)
         "r"(phase)
         : "memory");
     float y[128];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float4 v = *reinterpret_cast<const float4*>(myrow + 4 * i);
-      y[4 * i] = v.x;
-      y[4 * i + 1] = v.y;
-      y[4 * i + 2] = v.z;
-      y[4 * i + 3] = v.w;
-    }
+    load_elems<DT, 128>(y, myrow);  // exact widening of fp16 / bf16 keys
     const bool live = lane < nk;
 
     // ---- gamma: sequential fp64 sum of squares (codec.hpp:219-221) -----------
@@ -381,37 +376,49 @@ __global__ void __launch_bounds__(kCFThreads, 1)
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-template <int BD, int BN, int MODE>
-static cudaError_t launch_cf(const OqCodecParams& p, const float* x, size_t n, uint8_t* out,
-                             uint32_t* flag_idx, uint32_t* flag_cnt, cudaStream_t st,
-                             int num_sms) {
+template <int BD, int BN, int MODE, int DT>
+static cudaError_t launch_cf_t(const OqCodecParams& p, const void* x, size_t n, uint8_t* out,
+                               uint32_t* flag_idx, uint32_t* flag_cnt, cudaStream_t st,
+                               int num_sms) {
   using S = CFS<BD, BN>;
-  cudaError_t e = cudaFuncSetAttribute(compress_fast_kernel<BD, BN, MODE>,
+  cudaError_t e = cudaFuncSetAttribute(compress_fast_kernel<BD, BN, MODE, DT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
   if (e != cudaSuccess) return e;
   const size_t nblk = (n + 31) / 32;
   size_t grid = (nblk + kCFWarps - 1) / kCFWarps;
   if (grid > (size_t)num_sms) grid = num_sms;
-  compress_fast_kernel<BD, BN, MODE>
+  compress_fast_kernel<BD, BN, MODE, DT>
       <<<(unsigned)grid, kCFThreads, S::SMEM, st>>>(p, x, n, out, flag_idx, flag_cnt);
   return cudaGetLastError();
 }
 
+template <int BD, int BN, int MODE>
+static cudaError_t launch_cf(const OqCodecParams& p, const void* x, int dtype, size_t n,
+                             uint8_t* out, uint32_t* flag_idx, uint32_t* flag_cnt,
+                             cudaStream_t st, int num_sms) {
+  if (dtype == OQ_BF16)
+    return launch_cf_t<BD, BN, MODE, OQ_BF16>(p, x, n, out, flag_idx, flag_cnt, st, num_sms);
+  if (dtype == OQ_F16)
+    return launch_cf_t<BD, BN, MODE, OQ_F16>(p, x, n, out, flag_idx, flag_cnt, st, num_sms);
+  return launch_cf_t<BD, BN, MODE, OQ_F32>(p, x, n, out, flag_idx, flag_cnt, st, num_sms);
+}
+
 bool compress_fast_ok(const OqCodecParams& p, int dtype, const void* x, const void* out) {
-  if (p.dim != 128 || p.qjl || dtype != OQ_F32) return false;
+  if (p.dim != 128 || p.qjl || dtype == OQ_F64) return false;
   if (p.rounding != 0 && p.rounding != 2) return false;
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(out) & 15)) return false;
   return (p.b_dir == 3 && p.b_nrm == 1) || (p.b_dir == 4 && p.b_nrm == 2) ||
          (p.b_dir == 5 && p.b_nrm == 3);
 }
 
-cudaError_t launch_compress_fast(const OqCodecParams& p, const float* x, size_t n, uint8_t* out,
-                                 uint32_t* flag_idx, uint32_t* flag_cnt, cudaStream_t st,
-                                 int num_sms) {
-#define OQ_CF(BD, BN)                                                                      \
-  if (p.b_dir == BD && p.b_nrm == BN)                                                      \
-    return p.rounding == 0 ? launch_cf<BD, BN, 0>(p, x, n, out, flag_idx, flag_cnt, st, num_sms) \
-                           : launch_cf<BD, BN, 2>(p, x, n, out, flag_idx, flag_cnt, st, num_sms);
+cudaError_t launch_compress_fast(const OqCodecParams& p, const void* x, int dtype, size_t n,
+                                 uint8_t* out, uint32_t* flag_idx, uint32_t* flag_cnt,
+                                 cudaStream_t st, int num_sms) {
+#define OQ_CF(BD, BN)                                                                          \
+  if (p.b_dir == BD && p.b_nrm == BN)                                                          \
+    return p.rounding == 0                                                                     \
+               ? launch_cf<BD, BN, 0>(p, x, dtype, n, out, flag_idx, flag_cnt, st, num_sms)   \
+               : launch_cf<BD, BN, 2>(p, x, dtype, n, out, flag_idx, flag_cnt, st, num_sms);
   OQ_CF(3, 1)
   OQ_CF(4, 2)
   OQ_CF(5, 3)

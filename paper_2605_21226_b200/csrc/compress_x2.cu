@@ -1,4 +1,4 @@
-// compress_x2.cu — K1 for d = 128: Encoder::encode (codec.hpp:214-249), bit-
+// compress_x2.cu — K1 for d = 128 (fp32 / fp16 / bf16 keys): Encoder::encode (codec.hpp:214-249), bit-
 // exact in ONE pass, two lanes per key.
 //
 // Per warp, 16 keys at a time:
@@ -83,15 +83,15 @@ __device__ __forceinline__ uint32_t x2_bucket(double x, const float4* lut, const
   int cell = __float2int_rd(((float)x + 1.f) * (0.5f * kX2Cells));
   cell = cell < 0 ? 0 : (cell > kX2Cells - 1 ? kX2Cells - 1 : cell);
   const int lo = __float_as_int(lut[cell * kX2LutRep].x);
-  if (lo >= 0) return (uint32_t)lo + (x >= b64[lo + 1] ? 1u : 0u);
-  return quantize_ub(b64 + 1, (uint32_t)(K - 1), x);
+  if (lo >= 0 && x == x) return (uint32_t)lo + (x >= b64[lo + 1] ? 1u : 0u);
+  return quantize_ub(b64 + 1, (uint32_t)(K - 1), x);  // wide cells and NaN (inf keys)
 }
 
 // list != nullptr: encode only keys list[0 .. *list_n) (the certified-fp32
 // pass's flagged keys), each record stored at its own key slot.
-template <int BD, int BN, int MODE>
+template <int BD, int BN, int MODE, int DT>
 __global__ void __launch_bounds__(kX2Threads, 1)
-    compress_x2_kernel(OqCodecParams p, const float* __restrict__ x, size_t n,
+    compress_x2_kernel(OqCodecParams p, const void* __restrict__ x, size_t n,
                        uint8_t* __restrict__ out, const uint32_t* __restrict__ list,
                        const uint32_t* __restrict__ list_n) {
   using S = X2S<BD, BN>;
@@ -158,16 +158,18 @@ __global__ void __launch_bounds__(kX2Threads, 1)
   auto request = [&](size_t blk) {
     const size_t k0 = blk * 16;
     const int nk = (int)min((size_t)16, n - k0);
+    constexpr int EB = InElem<DT>::BYTES;
     if (lane == 0)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(x2_smem(bar)),
-                   "r"(nk * 512)
+                   "r"(nk * 128 * EB)
                    : "memory");
     __syncwarp();
     if (pk < nk)
       asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, "
-          "[%2];" ::"r"(x2_smem(half)),
-          "l"(x + key_of(k0 + pk) * 128 + 64 * h), "r"(x2_smem(bar))
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+          "[%3];" ::"r"(x2_smem(half)),
+          "l"(static_cast<const uint8_t*>(x) + (key_of(k0 + pk) * 128 + 64 * h) * EB),
+          "n"(64 * EB), "r"(x2_smem(bar))
           : "memory");
   };
   size_t blk = (size_t)blockIdx.x * kX2Warps + warp;
@@ -182,14 +184,7 @@ __global__ void __launch_bounds__(kX2Threads, 1)
         "r"(phase)
         : "memory");
     float y[64];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float4 v = *reinterpret_cast<const float4*>(half + 4 * i);
-      y[4 * i] = v.x;
-      y[4 * i + 1] = v.y;
-      y[4 * i + 2] = v.z;
-      y[4 * i + 3] = v.w;
-    }
+    load_elems<DT, 64>(y, half);  // exact widening of fp16 / bf16 keys
     __syncwarp();  // staging consumed: the work rows may overwrite it
 
     // ---- gamma = sqrt(sequential fp64 sum of squares) (codec.hpp:219-221) ----
@@ -300,6 +295,8 @@ __global__ void __launch_bounds__(kX2Threads, 1)
             const uint32_t a0 = sx > 0 ? sx - 1 : 0, a1 = sx + 1 < (uint32_t)K ? sx + 1 : K - 1;
             const uint32_t c0 = sy > 0 ? sy - 1 : 0, c1 = sy + 1 < (uint32_t)K ? sy + 1 : K - 1;
             double best = -INFINITY;
+            ix = a0;  // the reference's initial (bx, by) (codec.hpp:180-189)
+            iy = c0;
             for (uint32_t a = a0; a <= a1; ++a)
               for (uint32_t b = c0; b <= c1; ++b) {
                 const double* nd = dirs64 + 3 * (a * K + b);
@@ -396,30 +393,42 @@ __global__ void __launch_bounds__(kX2Threads, 1)
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-template <int BD, int BN, int MODE>
-static cudaError_t launch_x2(const OqCodecParams& p, const float* x, size_t n, uint8_t* out,
-                             cudaStream_t st, int num_sms, const uint32_t* list,
-                             const uint32_t* list_n) {
+template <int BD, int BN, int MODE, int DT>
+static cudaError_t launch_x2_t(const OqCodecParams& p, const void* x, size_t n, uint8_t* out,
+                               cudaStream_t st, int num_sms, const uint32_t* list,
+                               const uint32_t* list_n) {
   using S = X2S<BD, BN>;
   static_assert(S::SMEM <= 227 * 1024, "shared memory budget");
-  cudaError_t e = cudaFuncSetAttribute(compress_x2_kernel<BD, BN, MODE>,
+  cudaError_t e = cudaFuncSetAttribute(compress_x2_kernel<BD, BN, MODE, DT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
   if (e != cudaSuccess) return e;
   const size_t nblk = (n + 15) / 16;
   size_t grid = (nblk + kX2Warps - 1) / kX2Warps;
   if (grid > (size_t)num_sms) grid = num_sms;
-  compress_x2_kernel<BD, BN, MODE>
+  compress_x2_kernel<BD, BN, MODE, DT>
       <<<(unsigned)grid, kX2Threads, S::SMEM, st>>>(p, x, n, out, list, list_n);
   return cudaGetLastError();
 }
 
-cudaError_t launch_compress_x2(const OqCodecParams& p, const float* x, size_t n, uint8_t* out,
-                               cudaStream_t st, int num_sms, const uint32_t* list,
+template <int BD, int BN, int MODE>
+static cudaError_t launch_x2(const OqCodecParams& p, const void* x, int dtype, size_t n,
+                             uint8_t* out, cudaStream_t st, int num_sms, const uint32_t* list,
+                             const uint32_t* list_n) {
+  if (dtype == OQ_BF16)
+    return launch_x2_t<BD, BN, MODE, OQ_BF16>(p, x, n, out, st, num_sms, list, list_n);
+  if (dtype == OQ_F16)
+    return launch_x2_t<BD, BN, MODE, OQ_F16>(p, x, n, out, st, num_sms, list, list_n);
+  return launch_x2_t<BD, BN, MODE, OQ_F32>(p, x, n, out, st, num_sms, list, list_n);
+}
+
+cudaError_t launch_compress_x2(const OqCodecParams& p, const void* x, int dtype, size_t n,
+                               uint8_t* out, cudaStream_t st, int num_sms, const uint32_t* list,
                                const uint32_t* list_n) {
-#define OQ_X2(BD, BN)                                                                         \
-  if (p.b_dir == BD && p.b_nrm == BN)                                                         \
-    return p.rounding == 0 ? launch_x2<BD, BN, 0>(p, x, n, out, st, num_sms, list, list_n)    \
-                           : launch_x2<BD, BN, 2>(p, x, n, out, st, num_sms, list, list_n);
+#define OQ_X2(BD, BN)                                                                             \
+  if (p.b_dir == BD && p.b_nrm == BN)                                                             \
+    return p.rounding == 0                                                                        \
+               ? launch_x2<BD, BN, 0>(p, x, dtype, n, out, st, num_sms, list, list_n)             \
+               : launch_x2<BD, BN, 2>(p, x, dtype, n, out, st, num_sms, list, list_n);
   OQ_X2(3, 1)
   OQ_X2(4, 2)
   OQ_X2(5, 3)

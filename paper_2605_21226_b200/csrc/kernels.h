@@ -16,12 +16,12 @@ cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, si
                             uint8_t* out, cudaStream_t st, int num_sms,
                             uint32_t* flagged = nullptr);
 bool compress_fast_ok(const OqCodecParams& p, int dtype, const void* x, const void* out);
-cudaError_t launch_compress_x2(const OqCodecParams& p, const float* x, size_t n, uint8_t* out,
-                               cudaStream_t st, int num_sms, const uint32_t* list = nullptr,
-                               const uint32_t* list_n = nullptr);
-cudaError_t launch_compress_fast(const OqCodecParams& p, const float* x, size_t n, uint8_t* out,
-                                 uint32_t* flag_idx, uint32_t* flag_cnt, cudaStream_t st,
-                                 int num_sms);
+cudaError_t launch_compress_x2(const OqCodecParams& p, const void* x, int dtype, size_t n,
+                               uint8_t* out, cudaStream_t st, int num_sms,
+                               const uint32_t* list = nullptr, const uint32_t* list_n = nullptr);
+cudaError_t launch_compress_fast(const OqCodecParams& p, const void* x, int dtype, size_t n,
+                                 uint8_t* out, uint32_t* flag_idx, uint32_t* flag_cnt,
+                                 cudaStream_t st, int num_sms);
 // K2: Encoder::decode of OCTO v1 records -> fp32 [n, dim].
 cudaError_t launch_decode(const OqCodecParams& p, const uint8_t* recs, size_t n, float* out,
                           cudaStream_t st, int num_sms);

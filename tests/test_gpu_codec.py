@@ -154,3 +154,24 @@ def test_rejects_dimension_mismatch(cuda):
     import torch
     with pytest.raises(ValueError):
         oq.Encoder(oq.CodecConfig()).compress(torch.zeros((2, 64), device=cuda))
+
+
+@pytest.mark.parametrize("dtype", ["bfloat16", "float16"])
+@pytest.mark.parametrize("b,rounding", [(2, "local3x3"), (3, "local3x3"), (4, "local3x3"),
+                                        (3, "scalar")])
+def test_fast_path_16bit_keys_bit_exact(orc, cuda, dtype, b, rounding):
+    """The certified fast path (K1a + K1b) on bf16 / fp16 keys, as a decoder
+    appends them: 2^17 keys, bit-exact vs the CPU reference on the widened
+    values."""
+    import torch
+    n = 1 << 17
+    bd, bn = oq.default_bit_split(b)
+    g = torch.Generator(device=cuda).manual_seed(300 + b)
+    x = (torch.randn((n, 128), device=cuda, generator=g) * 3.0).to(getattr(torch, dtype))
+    enc = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rounding=rounding))
+    fl = torch.zeros(1, dtype=torch.int32, device=cuda)
+    got = enc.compress(x, flagged=fl).cpu().numpy()
+    want = orc.encoder(b_dir=bd, b_nrm=bn, rounding=rounding).encode_f32(
+        x.float().cpu().numpy(), threads=os.cpu_count() or 8)
+    bad = int((got != want).any(1).sum())
+    assert bad == 0, f"{bad} of {n} records differ ({int(fl.item())} flagged)"
