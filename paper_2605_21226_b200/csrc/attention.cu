@@ -54,10 +54,14 @@ constexpr int kPartW = 132;  // (m, l, 0, 0, acc[128]): acc 16-byte aligned
 // that own a word there (K: the 24 lanes c < 3, compacted as 3g + c; V: the
 // 28 lanes g < 7).
 __host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
-__host__ __device__ inline int kw_full(int W) { return cdiv(44 * W, 32); }
-__host__ __device__ inline int kw_3(int W) { return cdiv(40 * W, 32); }
-__host__ __device__ inline int vw_full(int W) { return cdiv(48 * W, 32); }
-__host__ __device__ inline int vw_7(int W) { return cdiv(8 * W, 32); }
+// Field width of a W-bit joint code in the lane runs: codes of W <= 8 bits
+// take one whole byte each, so one PRMT turns a code into its table address
+// (see code_addr); wider codes are packed back to back.
+__host__ __device__ constexpr int fw(int W) { return W <= 8 ? 8 : W; }
+__host__ __device__ inline int kw_full(int W) { return cdiv(44 * fw(W), 32); }
+__host__ __device__ inline int kw_3(int W) { return cdiv(40 * fw(W), 32); }
+__host__ __device__ inline int vw_full(int W) { return cdiv(48 * fw(W), 32); }
+__host__ __device__ inline int vw_7(int W) { return cdiv(8 * fw(W), 32); }
 __host__ __device__ inline int kcode_words(int W) { return 8 * (3 * kw_full(W) + kw_3(W)); }
 __host__ __device__ inline int vcode_words(int W) { return 28 * vw_full(W) + 4 * vw_7(W); }
 __host__ __device__ inline int ktile_bytes(int W, int qjl) {
@@ -127,8 +131,16 @@ __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
   return d;
 }
 
+// Byte-coded runs (W <= 8): the table sits at shared address 0x10000 with a
+// 256-byte entry stride (32 lane replicas of 8 bytes), and off = 0x10000 |
+// 8 * lane, so byte s % 4 of the run word is the address's byte 1:
+// address = 0x10000 | code << 8 | 8 * lane in ONE PRMT.
 template <int W, int N>
 __device__ __forceinline__ uint32_t code_addr(const uint32_t (&w)[N], int slot, uint32_t off) {
+  if constexpr (W <= 8) {
+    const int i = slot >> 2, b = slot & 3;
+    return __byte_perm(w[i], off, 0x7604 | (b << 4));
+  }
   const int pos = slot * W, i = pos >> 5, sh = pos & 31;
   constexpr uint32_t M = (1u << W) - 1u;
   if (sh + W <= 32) {
@@ -225,13 +237,16 @@ struct AttnKParams {
 
 template <int W, bool QJL>
 struct Cfg {
-  static constexpr int KWF = (44 * W + 31) / 32, KW3 = (40 * W + 31) / 32;
-  static constexpr int VWF = (48 * W + 31) / 32, VW7 = (8 * W + 31) / 32;
+  static constexpr int FW = W <= 8 ? 8 : W;  // stored field width
+  static constexpr int KWF = (44 * FW + 31) / 32, KW3 = (40 * FW + 31) / 32;
+  static constexpr int VWF = (48 * FW + 31) / 32, VW7 = (8 * FW + 31) / 32;
   static constexpr int KCODE = 8 * (3 * KWF + KW3), VCODE = 28 * VWF + 4 * VW7;
   static constexpr int KTILE = (128 + 4 * KCODE + (QJL ? 576 : 0) + 15) & ~15;
   static constexpr int VTILE = (128 + 4 * VCODE + 15) & ~15;
   static constexpr int QF = 18 + (QJL ? 16 : 0);
-  static constexpr int TAB_BYTES = (1 << W) * 16 * 8;
+  // W <= 8: the table lives at shared address 0x10000 (256-byte entries);
+  // TAB_BYTES then spans from the start of dynamic smem to its end
+  static constexpr int TAB_BYTES = W <= 8 ? 0x10000 + (1 << W) * 256 : (1 << W) * 16 * 8;
   static constexpr int QS_FLOATS = 8 * 2 * 129;  // fused query prep scratch
   static constexpr int smem(int nw) { return TAB_BYTES + nw * 8 * kPartW * 4 + QS_FLOATS * 4; }
 };
@@ -682,9 +697,18 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, c = lane & 3;
 
-  for (int i = tid; i < (1 << W) * 16; i += blockDim.x) tab[i] = P.tab[i >> 4];
-  const uint32_t toff =
-      static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + ((lane & 15) << 3);
+  uint32_t toff;
+  if constexpr (W <= 8) {
+    // table at shared address 0x10000: 32 replicas x 8 B per entry
+    const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    if (base > 0x10000u) __trap();
+    uint2* t8 = reinterpret_cast<uint2*>(smem + (0x10000u - base));
+    for (int i = tid; i < (1 << W) * 32; i += blockDim.x) t8[i] = P.tab[i >> 5];
+    toff = 0x10000u | ((uint32_t)lane << 3);
+  } else {
+    for (int i = tid; i < (1 << W) * 16; i += blockDim.x) tab[i] = P.tab[i >> 4];
+    toff = static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + ((lane & 15) << 3);
+  }
   __syncthreads();
 
   auto run = [&](const Seg& it, int nparts) {
@@ -943,13 +967,14 @@ __global__ void pack_tiles_kernel(OqCodecParams p, int role, const uint8_t* __re
       const uint8_t* r = rec(v_token(c, k));
       code = r ? rec_joint(p, r, 6 * g + u) : 0u;
     }
-    // append W bits LSB-first
+    // append FW bits LSB-first
+    const int FWb = fw(W);
     acc |= code << nbits;
-    nbits += W;
+    nbits += FWb;
     if (nbits >= 32) {
       put(wi++, acc);
       nbits -= 32;
-      acc = nbits ? code >> (W - nbits) : 0u;
+      acc = nbits ? code >> (FWb - nbits) : 0u;
     }
   }
   if (nbits) put(wi++, acc);
@@ -981,6 +1006,7 @@ __global__ void pack_tiles_kernel(OqCodecParams p, int role, const uint8_t* __re
 // slots write.  Same bit layout as pack_tiles_kernel.
 __device__ __forceinline__ void put_field(uint32_t* codes, int W, int lane, int role, int slot,
                                           uint32_t code) {
+  W = fw(W);  // stored field width
   const int pos = slot * W, i = pos >> 5, sh = pos & 31;
   auto word = [&](int wi) -> uint32_t& {
     return codes[role == 0 ? k_word_off(W, lane, wi) : v_word_off(W, lane, wi)];
