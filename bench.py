@@ -362,6 +362,59 @@ def main():
     clk.__exit__(None, None, None)
     e2e_val = world * alg_bytes_rank * args.steps / (e2e_ms * 1e-3) / 1e9
 
+    # ---- one decoder step: append the new token's K and V of every stream ------
+    # (compress + write into its tile slot), then attention over T+1 tokens
+    step_info = None
+    if world == 1 and not args.no_compress:
+        kn = torch.randn((B, Hkv, 128), device=dev).to(torch.bfloat16)
+        vn = torch.randn((B, Hkv, 128), device=dev).to(torch.bfloat16)
+        pos = T - 1  # overwrite the last slot: the cache keeps its size
+        for _ in range(3):
+            cache.append(kn, vn, pos=pos)
+        torch.cuda.synchronize()
+        a0, a1, a2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a0.record(stream)
+        for _ in range(args.steps):
+            cache.append(kn, vn, pos=pos)
+        a1.record(stream)
+        for _ in range(args.steps):
+            cache.append(kn, vn, pos=pos)
+            step(q)
+        a2.record(stream)
+        torch.cuda.synchronize()
+        ap = a0.elapsed_time(a1) / args.steps
+        st = a1.elapsed_time(a2) / args.steps
+        step_info = {"what": "decoder step: bf16 K/V of B*Hkv streams appended (K1 + tile insert, "
+                             "per role) then decode attention over the 128K-token cache",
+                     "append_us": ap * 1e3, "append_plus_attention_us": st * 1e3}
+        # the same step captured once in a CUDA graph and replayed (how a serving
+        # loop removes the per-launch host overhead of the small append kernels)
+        try:
+            gs = torch.cuda.Stream()
+            gs.wait_stream(stream)
+            with torch.cuda.stream(gs):
+                for _ in range(2):
+                    cache.append(kn, vn, pos=pos)
+                    step(q)
+            torch.cuda.current_stream().wait_stream(gs)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                cache.append(kn, vn, pos=pos)
+                step(q)
+            for _ in range(3):
+                graph.replay()
+            torch.cuda.synchronize()
+            g0, g1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            g0.record(stream)
+            for _ in range(args.steps):
+                graph.replay()
+            g1.record(stream)
+            torch.cuda.synchronize()
+            step_info["graph_append_plus_attention_us"] = g0.elapsed_time(g1) / args.steps * 1e3
+        except Exception as e:  # pragma: no cover - reported, not fatal
+            step_info["graph_error"] = str(e)[:200]
+
     # ---- compress (BASELINE configs[1]: 2^20 keys, fp32 in) ----------------------
     comp = None
     if not args.no_compress:
@@ -414,6 +467,7 @@ def main():
             # merge + final merge around the NCCL all-gather
             "gpu_launches": (1 if world == 1 else 4) * args.steps,
             "compress": comp,
+            "decode_step": step_info,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -152,6 +152,35 @@ __device__ __forceinline__ uint32_t code_addr(const uint32_t (&w)[N], int slot, 
   return off + (v & (M << 7));
 }
 
+// Replicate the NE-entry joint table REP times into shared memory: every
+// thread first loads all of its entries (independent global loads in flight
+// together), then writes each entry's REP consecutive copies with 16-byte
+// stores.  (A strided copy loop serialises one L2 round trip per few entries,
+// which cost several microseconds per launch.)
+template <int REP, int NE>
+__device__ __forceinline__ void stage_table(uint2* dst, const uint2* __restrict__ src, int tid,
+                                            int nthreads) {
+  constexpr int MAXPT = 8;  // entries per thread per pass
+  for (int e0 = 0; e0 < NE; e0 += nthreads * MAXPT) {
+    uint2 v[MAXPT];
+#pragma unroll
+    for (int k = 0; k < MAXPT; ++k) {
+      const int e = e0 + k * nthreads + tid;
+      v[k] = e < NE ? __ldg(src + e) : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int k = 0; k < MAXPT; ++k) {
+      const int e = e0 + k * nthreads + tid;
+      if (e < NE) {
+        uint4* d = reinterpret_cast<uint4*>(dst + (size_t)e * REP);
+        const uint4 q = make_uint4(v[k].x, v[k].y, v[k].x, v[k].y);
+#pragma unroll
+        for (int r = 0; r < REP / 2; ++r) d[r] = q;
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ uint2 lds64(uint32_t addr) {
   uint2 r;
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(addr));
@@ -703,10 +732,10 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
     const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     if (base > 0x10000u) __trap();
     uint2* t8 = reinterpret_cast<uint2*>(smem + (0x10000u - base));
-    for (int i = tid; i < (1 << W) * 32; i += blockDim.x) t8[i] = P.tab[i >> 5];
+    stage_table<32, (1 << W)>(t8, P.tab, tid, blockDim.x);
     toff = 0x10000u | ((uint32_t)lane << 3);
   } else {
-    for (int i = tid; i < (1 << W) * 16; i += blockDim.x) tab[i] = P.tab[i >> 4];
+    stage_table<16, (1 << W)>(tab, P.tab, tid, blockDim.x);
     toff = static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + ((lane & 15) << 3);
   }
   __syncthreads();
@@ -1004,29 +1033,17 @@ __global__ void pack_tiles_kernel(OqCodecParams p, int role, const uint8_t* __re
 // 31 tokens of the tile untouched (read-modify-write of the W-bit fields in
 // the lane runs).  One warp per stream; only the lanes owning that token's
 // slots write.  Same bit layout as pack_tiles_kernel.
-__device__ __forceinline__ void put_field(uint32_t* codes, int W, int lane, int role, int slot,
-                                          uint32_t code) {
-  W = fw(W);  // stored field width
-  const int pos = slot * W, i = pos >> 5, sh = pos & 31;
-  auto word = [&](int wi) -> uint32_t& {
-    return codes[role == 0 ? k_word_off(W, lane, wi) : v_word_off(W, lane, wi)];
-  };
-  const uint32_t m = (1u << W) - 1u;
-  uint32_t& w0 = word(i);
-  w0 = (w0 & ~(m << sh)) | (code << sh);
-  if (sh + W > 32) {
-    uint32_t& w1 = word(i + 1);
-    const int hi = sh + W - 32;
-    w1 = (w1 & ~((1u << hi) - 1u)) | (code >> (W - hi));
-  }
-}
-
-__global__ void append_token_kernel(OqCodecParams p, int role, const uint8_t* __restrict__ recs,
-                                    size_t n_streams, const int64_t* __restrict__ pos_dev,
-                                    int64_t pos_scalar, uint8_t* __restrict__ tiles,
-                                    size_t tiles_cap) {
+__global__ void __launch_bounds__(256) append_token_kernel(
+    OqCodecParams p, int role, const uint8_t* __restrict__ recs, size_t n_streams,
+    const int64_t* __restrict__ pos_dev, int64_t pos_scalar, uint8_t* __restrict__ tiles,
+    size_t tiles_cap) {
+  // per warp: the stream's record, and each writing lane's run words, staged
+  // in shared memory so that the read-modify-writes of the W-bit fields cost
+  // one batch of global loads and one of stores instead of a round trip each
+  __shared__ uint32_t rec_s[8][32];
+  __shared__ uint32_t run_s[8][32][21];
   const int W = 2 * p.b_dir + p.b_nrm;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const size_t s = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
   if (s >= n_streams) return;
   const int64_t pos = pos_dev ? pos_dev[s] : pos_scalar;
@@ -1035,38 +1052,61 @@ __global__ void append_token_kernel(OqCodecParams p, int role, const uint8_t* __
   const int tt = (int)(pos % 32);
   const int tb = role == 0 ? ktile_bytes(W, p.qjl) : vtile_bytes(W);
   uint8_t* out = tiles + (s * tiles_cap + tile) * (size_t)tb;
-  const uint8_t* r = recs + s * p.rec_bytes;
+  {
+    const uint8_t* rg = recs + s * p.rec_bytes;
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t bi = 4 * lane + i;
+      if (bi < p.rec_bytes) w |= (uint32_t)rg[bi] << (8 * i);
+    }
+    rec_s[wib][lane] = w;
+  }
+  __syncwarp();
+  const uint8_t* r = reinterpret_cast<const uint8_t*>(rec_s[wib]);
   const int g = lane >> 2, c = lane & 3;
   const int tg = tt & 7, tk = tt >> 3;  // token = g + 8k in the K map and the gamma slots
-  if (lane == 0) {
-    const uint32_t b = (uint32_t)r[0] | ((uint32_t)r[1] << 8) | ((uint32_t)r[2] << 16) |
-                       ((uint32_t)r[3] << 24);
-    reinterpret_cast<float*>(out)[tg * 4 + tk] = __uint_as_float(b);
-  }
+  if (lane == 0)
+    reinterpret_cast<float*>(out)[tg * 4 + tk] = __uint_as_float(rec_s[wib][0]);
   uint32_t* codes = reinterpret_cast<uint32_t*>(out + 128);
+  const bool writer = role == 0 ? (g == tg) : (c == ((tt & 7) >> 1));
+  if (!writer) return;
+  const int nw = role == 0 ? (c < 3 ? kw_full(W) : kw_3(W)) : (g < 7 ? vw_full(W) : vw_7(W));
+  uint32_t* run = run_s[wib][lane];
+  auto woff = [&](int i) { return role == 0 ? k_word_off(W, lane, i) : v_word_off(W, lane, i); };
+#pragma unroll 4
+  for (int i = 0; i < nw; ++i) run[i] = codes[woff(i)];
+  const int FW = fw(W);
+  const uint32_t m = (1u << FW) - 1u;
+  auto put = [&](int slot, uint32_t code) {
+    const int bpos = slot * FW, i = bpos >> 5, sh = bpos & 31;
+    run[i] = (run[i] & ~(m << sh)) | (code << sh);
+    if (sh + FW > 32) {
+      const int hi = sh + FW - 32;
+      run[i + 1] = (run[i + 1] & ~((1u << hi) - 1u)) | (code >> (FW - hi));
+    }
+  };
   if (role == 0) {
-    if (g == tg) {
-      const int nu = c < 3 ? 11 : 10;
-      for (int u = 0; u < nu; ++u) put_field(codes, W, lane, 0, u * 4 + tk, rec_joint(p, r, 11 * c + u));
-      if (p.qjl) {
-        uint8_t* qa = out + 128 + 4 * kcode_words(W);
-        const int sign_off = 4 + p.dir_bytes + p.nrm_bytes + 2;
-        if (c == 0)
-          reinterpret_cast<uint16_t*>(qa)[tg * 4 + tk] =
-              (uint16_t)(r[sign_off - 2] | (r[sign_off - 1] << 8));
-        uint32_t w = 0;
-        for (int i = 0; i < 4; ++i) w |= (uint32_t)r[sign_off + 4 * c + i] << (8 * i);
-        reinterpret_cast<uint32_t*>(qa + 64)[(4 * g + c) * 4 + tk] = w;
-      }
+    const int nu = c < 3 ? 11 : 10;
+    for (int u = 0; u < nu; ++u) put(u * 4 + tk, rec_joint(p, r, 11 * c + u));
+    if (p.qjl) {
+      uint8_t* qa = out + 128 + 4 * kcode_words(W);
+      const int sign_off = 4 + p.dir_bytes + p.nrm_bytes + 2;
+      if (c == 0)
+        reinterpret_cast<uint16_t*>(qa)[tg * 4 + tk] =
+            (uint16_t)(r[sign_off - 2] | (r[sign_off - 1] << 8));
+      uint32_t w = 0;
+      for (int i = 0; i < 4; ++i) w |= (uint32_t)r[sign_off + 4 * c + i] << (8 * i);
+      reinterpret_cast<uint32_t*>(qa + 64)[(4 * g + c) * 4 + tk] = w;
     }
   } else {
     // V map: token v_token(c, k) = 16 (k >> 2) + 2c + (k & 1) + 8 ((k >> 1) & 1)
-    if (c == ((tt & 7) >> 1)) {
-      const int k = (tt >> 4) * 4 + ((tt >> 3) & 1) * 2 + (tt & 1);
-      const int nu = g < 7 ? 6 : 1;
-      for (int u = 0; u < nu; ++u) put_field(codes, W, lane, 1, u * 8 + k, rec_joint(p, r, 6 * g + u));
-    }
+    const int k = (tt >> 4) * 4 + ((tt >> 3) & 1) * 2 + (tt & 1);
+    const int nu = g < 7 ? 6 : 1;
+    for (int u = 0; u < nu; ++u) put(u * 8 + k, rec_joint(p, r, 6 * g + u));
   }
+#pragma unroll 4
+  for (int i = 0; i < nw; ++i) codes[woff(i)] = run[i];
 }
 
 cudaError_t launch_append_token(const OqCodecParams& p, int role, const uint8_t* recs,
@@ -1168,8 +1208,7 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
     const size_t U = (size_t)P.n_sh * P.tps;
     grid = (int)(U < (size_t)num_sms ? (U ? U : 1) : num_sms);
   }
-  cudaError_t e = cudaFuncSetAttribute(attn_partials_kernel<W, QJL, NW>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem(NW));
+  cudaError_t e = set_smem_once(attn_partials_kernel<W, QJL, NW>, C::smem(NW));
   if (e != cudaSuccess) return e;
   attn_partials_kernel<W, QJL, NW><<<grid, NW * 32, C::smem(NW), st>>>(P);
   return cudaGetLastError();

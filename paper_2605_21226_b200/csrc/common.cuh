@@ -1,6 +1,9 @@
 // common.cuh — shared device helpers for the sm_100a OCTOPUS kernels.
 #pragma once
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -69,6 +72,47 @@ __device__ __forceinline__ double load_as_double(const void* p, int dtype, size_
     default: {  // OQ_BF16
       const uint16_t b = static_cast<const uint16_t*>(p)[i];
       return (double)__uint_as_float((uint32_t)b << 16);
+    }
+  }
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel, device
+// and size: it costs microseconds, which matters for decode-step launches.
+inline cudaError_t set_smem_once(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> bytes set
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{fn, dev}];
+  if (have >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+template <typename F>
+inline cudaError_t set_smem_once(F* fn, int bytes) {
+  return set_smem_once(reinterpret_cast<const void*>(fn), bytes);
+}
+
+// Fill REP consecutive shared copies of NCELL float4 cells, cell i = f(i)
+// (f may read global memory): every thread first evaluates all of its cells
+// (independent loads in flight together), then stores the replicas.
+template <int REP, int NCELL, int PER = 8, typename F>
+__device__ __forceinline__ void stage_cells(float4* dst, F f, int tid, int nthreads) {
+  for (int c0 = 0; c0 < NCELL; c0 += nthreads * PER) {
+    float4 v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int c = c0 + k * nthreads + tid;
+      v[k] = c < NCELL ? f(c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int c = c0 + k * nthreads + tid;
+      if (c < NCELL)
+#pragma unroll
+        for (int r = 0; r < REP; ++r) dst[c * REP + r] = v[k];
     }
   }
 }

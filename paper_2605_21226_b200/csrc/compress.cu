@@ -475,8 +475,7 @@ static cudaError_t launch_compress_dt(const OqCodecParams& p, const void* x, int
                                      const uint32_t* list, const uint32_t* list_n) {
   using S = CompressShape<D>;
   const size_t smem = compress_smem<D>(p);
-  cudaError_t e = cudaFuncSetAttribute(compress_kernel<D, TAB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_once(compress_kernel<D, TAB>, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compress_kernel<D, TAB>, S::THREADS, smem);
@@ -513,6 +512,13 @@ cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, si
     if (!e) return 1;
     return e[0] == 'x' ? 0 : (e[0] == 'e' ? 2 : 1);
   }();
+  // small batches (a decode step appends B*Hkv keys): the exact two-lanes-
+  // per-key kernel alone, one launch, no flagged-key list
+  if (impl == 1 && n <= 8192 && compress_fast_ok(p, dtype, x, out)) {
+    cudaError_t e = flagged ? cudaMemsetAsync(flagged, 0, sizeof(uint32_t), st) : cudaSuccess;
+    if (e == cudaSuccess) e = launch_compress_x2(p, x, dtype, n, out, st, num_sms);
+    return e;
+  }
   if (impl == 0 && compress_fast_ok(p, dtype, x, out)) {
     cudaError_t e = flagged ? cudaMemsetAsync(flagged, 0, sizeof(uint32_t), st) : cudaSuccess;
     if (e == cudaSuccess)

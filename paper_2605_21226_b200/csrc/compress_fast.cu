@@ -105,15 +105,15 @@ __global__ void __launch_bounds__(kCFThreads, 1)
   // cell (a + 1, b + 1) = (n_hat(a, b), bias 0); border cells (0, 0, 0, -inf)
   // so every 3x3 window is 9 loads at immediate offsets and out-of-range
   // candidates score -inf (codec.hpp:164-176 clamps the window)
-  for (int i = tid; i < S::KP * S::KP * S::DREP; i += kCFThreads) {
-    const int cell = i / S::DREP, a = cell / S::KP - 1, b = cell % S::KP - 1;
+  stage_cells<S::DREP, S::KP * S::KP>(dirs, [&](int cell) {
+    const int a = cell / S::KP - 1, b = cell % S::KP - 1;
     float4 v = make_float4(0.f, 0.f, 0.f, -INFINITY);
     if (a >= 0 && a < K && b >= 0 && b < K) {
-      v = reinterpret_cast<const float4*>(p.dirs32)[a * K + b];
+      v = __ldg(reinterpret_cast<const float4*>(p.dirs32) + a * K + b);
       v.w = 0.f;
     }
-    dirs[i] = v;
-  }
+    return v;
+  }, tid, kCFThreads);
   if (tid <= K) bnd[tid] = tid == 0 ? -INFINITY : (tid == K ? INFINITY : (float)p.xi_bnd[tid - 1]);
   __syncthreads();
   for (int c = tid; c < kCFCells; c += kCFThreads) {
@@ -381,8 +381,7 @@ static cudaError_t launch_cf_t(const OqCodecParams& p, const void* x, size_t n, 
                                uint32_t* flag_idx, uint32_t* flag_cnt, cudaStream_t st,
                                int num_sms) {
   using S = CFS<BD, BN>;
-  cudaError_t e = cudaFuncSetAttribute(compress_fast_kernel<BD, BN, MODE, DT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+  cudaError_t e = set_smem_once(compress_fast_kernel<BD, BN, MODE, DT>, S::SMEM);
   if (e != cudaSuccess) return e;
   const size_t nblk = (n + 31) / 32;
   size_t grid = (nblk + kCFWarps - 1) / kCFWarps;

@@ -111,16 +111,29 @@ __global__ void __launch_bounds__(kX2Threads, 1)
   // ---- tables -------------------------------------------------------------
   // padded fp32 direction grid: cell (a + 1, b + 1) = (n_hat(a, b), 0),
   // border cells (0, 0, 0, -inf): out-of-window candidates score -inf
-  for (int i = tid; i < S::KP * S::KP * S::DREP; i += kX2Threads) {
-    const int cell = i / S::DREP, a = cell / S::KP - 1, b = cell % S::KP - 1;
+  stage_cells<S::DREP, S::KP * S::KP>(dirs32, [&](int cell) {
+    const int a = cell / S::KP - 1, b = cell % S::KP - 1;
     float4 v = make_float4(0.f, 0.f, 0.f, -INFINITY);
     if (a >= 0 && a < K && b >= 0 && b < K) {
-      v = reinterpret_cast<const float4*>(p.dirs32)[a * K + b];
+      v = __ldg(reinterpret_cast<const float4*>(p.dirs32) + a * K + b);
       v.w = 0.f;
     }
-    dirs32[i] = v;
+    return v;
+  }, tid, kX2Threads);
+  {
+    constexpr int N64 = K * K * 3, PER = (N64 + kX2Threads - 1) / kX2Threads;
+    double v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = k * kX2Threads + tid;
+      v[k] = i < N64 ? __ldg(p.dirs64 + i) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = k * kX2Threads + tid;
+      if (i < N64) dirs64[i] = v[k];
+    }
   }
-  for (int i = tid; i < K * K * 3; i += kX2Threads) dirs64[i] = p.dirs64[i];
   if (tid <= K) b64[tid] = tid == 0 ? -INFINITY : (tid == K ? INFINITY : p.xi_bnd[tid - 1]);
   __syncthreads();
   for (int c = tid; c < kX2Cells; c += kX2Threads) {
@@ -399,8 +412,7 @@ static cudaError_t launch_x2_t(const OqCodecParams& p, const void* x, size_t n, 
                                const uint32_t* list_n) {
   using S = X2S<BD, BN>;
   static_assert(S::SMEM <= 227 * 1024, "shared memory budget");
-  cudaError_t e = cudaFuncSetAttribute(compress_x2_kernel<BD, BN, MODE, DT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+  cudaError_t e = set_smem_once(compress_x2_kernel<BD, BN, MODE, DT>, S::SMEM);
   if (e != cudaSuccess) return e;
   const size_t nblk = (n + 15) / 16;
   size_t grid = (nblk + kX2Warps - 1) / kX2Warps;

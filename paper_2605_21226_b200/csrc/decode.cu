@@ -299,10 +299,13 @@ __global__ void __launch_bounds__(kD128Threads, 3) decode128_kernel(OqCodecParam
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // direction table in field-pair order pr = ixi | ieta << b_dir
-  for (int i = tid; i < S::NPAIR * S::REP; i += kD128Threads) {
-    const int pr = i / S::REP, a = pr & ((1 << BD) - 1), b = pr >> BD;
-    dirs_s[i] = reinterpret_cast<const float4*>(p.dirs32)[(a << BD) | b];
-  }
+  stage_cells<S::REP, S::NPAIR>(
+      dirs_s,
+      [&](int pr) {
+        const int a = pr & ((1 << BD) - 1), b = pr >> BD;
+        return __ldg(reinterpret_cast<const float4*>(p.dirs32) + ((a << BD) | b));
+      },
+      tid, kD128Threads);
   for (int i = tid; i < S::NRHO; i += kD128Threads) rho_s[i] = p.rho32[i];
   const float4* dtab = dirs_s + (lane & (S::REP - 1));
   float* hs = half_s + warp * 32 * kD128HalfStride;
@@ -418,8 +421,7 @@ static cudaError_t launch_decode128(const OqCodecParams& p, const uint8_t* recs,
   using S = D128<BD, BN>;
   const size_t smem = (size_t)S::NPAIR * S::REP * 16 + 16 * 4 + 4 * 32 * kD128HalfStride * 4 +
                       16 + 2 * (((size_t)kD128Threads * p.rec_bytes + 15) & ~size_t(15)) + 64;
-  cudaError_t e = cudaFuncSetAttribute(decode128_kernel<BD, BN>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_once(decode128_kernel<BD, BN>, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode128_kernel<BD, BN>,
@@ -441,8 +443,7 @@ static cudaError_t launch_decode_dt(const OqCodecParams& p, const uint8_t* recs,
   const uint32_t kk = p.K * p.K;
   const size_t smem = (TAB ? kk * 16 * kDecRep : 0) + 256 * 4 +
                       (size_t)S::VPC * S::STRIDE * 4 + (size_t)S::VPC * p.rec_bytes + 64;
-  cudaError_t e = cudaFuncSetAttribute(decode_kernel<D, TAB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_once(decode_kernel<D, TAB>, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<D, TAB>, S::THREADS,
