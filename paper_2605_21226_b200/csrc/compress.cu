@@ -455,6 +455,91 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small batches (a decode step compresses one key per (batch, kv head)
+// stream): ONE WARP PER KEY, latency first.  Lane l holds coordinates
+// 4l .. 4l+3 in fp64; gamma is lane 0's sequential sum over the shared row
+// (codec.hpp:219-221); signs + WHT use the reference's butterfly pairs (two
+// in-lane stages, five shuffle stages); lane l then rounds triplets l and
+// l + 32 with joint_round reading the codec tables straight from global
+// memory (L1-resident: no per-CTA staging), and the fields are OR-ed into a
+// shared record.  d = 128, no QJL, any rounding mode and bit split.
+constexpr int kSmallWarps = 4;
+
+__global__ void __launch_bounds__(32 * kSmallWarps) compress_small_kernel(
+    OqCodecParams p, const void* __restrict__ x, int dtype, size_t n, uint8_t* __restrict__ out) {
+  __shared__ double row_s[kSmallWarps][132];
+  __shared__ uint32_t rec_s[kSmallWarps][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const size_t key = blockIdx.x * (size_t)kSmallWarps + wib;
+  if (key >= n) return;
+  double* row = row_s[wib];
+  uint32_t* rec = rec_s[wib];
+  double v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[i] = load_as_double(x, dtype, key * 128 + 4 * lane + i);
+    row[4 * lane + i] = dmul(v[i], v[i]);
+  }
+  rec[lane] = 0u;
+  __syncwarp();
+  double g2 = 0.0;  // squares are rounded identically in parallel: only the adds chain
+  if (lane == 0)
+    for (int e = 0; e < 128; ++e) g2 = dadd(g2, row[e]);
+  g2 = __shfl_sync(kFull, g2, 0);
+  const double gamma = dsqrt(g2);
+  const double inv = ddiv(1.0, gamma > 1e-12 ? gamma : 1e-12);
+  // u = k * inv, signs, fwht (rotation.hpp:20-31, 46-49)
+  const uint32_t sm = p.sign_mask[lane >> 3] >> (4 * (lane & 7));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = dflip(dmul(v[i], inv), (sm >> i) & 1u);
+  {
+    double a = v[0], b = v[1];
+    v[0] = dadd(a, b); v[1] = dsub(a, b);
+    a = v[2]; b = v[3];
+    v[2] = dadd(a, b); v[3] = dsub(a, b);
+    a = v[0]; b = v[2];
+    v[0] = dadd(a, b); v[2] = dsub(a, b);
+    a = v[1]; b = v[3];
+    v[1] = dadd(a, b); v[3] = dsub(a, b);
+  }
+#pragma unroll
+  for (int lm = 1; lm < 32; lm <<= 1) {
+    const bool up = lane & lm;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double o = __shfl_xor_sync(kFull, v[i], lm);
+      v[i] = up ? dsub(o, v[i]) : dadd(v[i], o);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) row[4 * lane + i] = dmul(v[i], p.inv_sqrt_d);
+  if (lane == 0) row[128] = 0.0;  // zero pad to 3 * n_tri (codec.hpp:229-230)
+  __syncwarp();
+  const CompressSmem tabs{const_cast<double*>(p.xi_bnd), const_cast<double*>(p.rho_bnd),
+                          const_cast<double*>(p.rho_c), p.dirs64, p.xi_lut, p.rho_lut};
+  const float4* d32 = reinterpret_cast<const float4*>(p.dirs32);
+  const int pb = 2 * p.b_dir, nb = p.b_nrm;
+  for (int t = lane; t < 43; t += 32) {
+    const uint32_t code = joint_round(p, tabs, d32, row[3 * t], row[3 * t + 1], row[3 * t + 2]);
+    const uint32_t pr = (code & 0xff) | (((code >> 8) & 0xff) << p.b_dir), ir = code >> 16;
+    // dir field pair t at bit 32 + pb t, norm field t at bit 32 + 8 dir_bytes + nb t
+    const int dp = 32 + pb * t, np = 32 + 8 * (int)p.dir_bytes + nb * t;
+    atomicOr(&rec[dp >> 5], pr << (dp & 31));
+    if ((dp & 31) + pb > 32) atomicOr(&rec[(dp >> 5) + 1], pr >> (32 - (dp & 31)));
+    atomicOr(&rec[np >> 5], ir << (np & 31));
+    if ((np & 31) + nb > 32) atomicOr(&rec[(np >> 5) + 1], ir >> (32 - (np & 31)));
+  }
+  __syncwarp();
+  if (lane == 0) rec[0] = __float_as_uint((float)gamma);  // codec.hpp:233
+  __syncwarp();
+  const uint32_t rb = p.rec_bytes;
+  uint8_t* dst = out + key * rb;
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(rec);
+  for (uint32_t b = lane; b < rb; b += 32) dst[b] = src[b];
+}
+
 template <int D>
 static size_t compress_smem(const OqCodecParams& p) {
   using S = CompressShape<D>;
@@ -512,8 +597,17 @@ cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, si
     if (!e) return 1;
     return e[0] == 'x' ? 0 : (e[0] == 'e' ? 2 : 1);
   }();
-  // small batches (a decode step appends B*Hkv keys): the exact two-lanes-
-  // per-key kernel alone, one launch, no flagged-key list
+  // small batches (a decode step appends B*Hkv keys): one warp per key,
+  // exact, one launch, no table staging
+  if (impl == 1 && n <= 2048 && p.dim == 128 && !p.qjl) {
+    cudaError_t e = flagged ? cudaMemsetAsync(flagged, 0, sizeof(uint32_t), st) : cudaSuccess;
+    if (e == cudaSuccess) {
+      compress_small_kernel<<<(unsigned)((n + kSmallWarps - 1) / kSmallWarps), 32 * kSmallWarps, 0,
+                              st>>>(p, x, dtype, n, out);
+      e = cudaGetLastError();
+    }
+    return e;
+  }
   if (impl == 1 && n <= 8192 && compress_fast_ok(p, dtype, x, out)) {
     cudaError_t e = flagged ? cudaMemsetAsync(flagged, 0, sizeof(uint32_t), st) : cudaSuccess;
     if (e == cudaSuccess) e = launch_compress_x2(p, x, dtype, n, out, st, num_sms);

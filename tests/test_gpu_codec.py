@@ -175,3 +175,27 @@ def test_fast_path_16bit_keys_bit_exact(orc, cuda, dtype, b, rounding):
         x.float().cpu().numpy(), threads=os.cpu_count() or 8)
     bad = int((got != want).any(1).sum())
     assert bad == 0, f"{bad} of {n} records differ ({int(fl.item())} flagged)"
+
+
+SMALL = [c for c in CONFIGS if c.get("dim", 128) == 128 and not c.get("qjl")]
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64", "bfloat16"])
+@pytest.mark.parametrize("cfg", SMALL, ids=_ids)
+def test_small_batch_kernel_bit_exact(orc, cuda, cfg, dtype):
+    """Batches of <= 2048 d=128 keys (a decode step's append) take the
+    one-warp-per-key kernel: bit-exact in every rounding mode and bit split,
+    ragged batch sizes included."""
+    import torch
+    for n in (1, 7, 777):
+        x = _inputs(orc, 5, max(n, 8), 128)[:n]
+        t = torch.from_numpy(x).to(cuda).to(getattr(torch, dtype))
+        if dtype == "float64":
+            t = t * (1.0 + 1e-9)  # off the fp32 grid: the squares round
+        xs = t.double().cpu().numpy()
+        got = oq.Encoder(oq.CodecConfig(**cfg)).compress(t).cpu().numpy()
+        eo = orc.encoder(**cfg)
+        want = np.stack([eo.encode_f64(k) for k in xs]) if dtype == "float64" else \
+            eo.encode_f32(xs.astype(np.float32))
+        bad = np.nonzero((got != want).any(1))[0]
+        assert bad.size == 0, f"n={n}: {bad.size} mismatching records, first {bad[:5]}"
