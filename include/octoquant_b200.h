@@ -135,6 +135,16 @@ typedef struct oq_attn_shape {
 oq_status oq_cache_append(const oq_codec* codec, int role, const void* x, int dtype,
                           uint64_t n_streams, const int64_t* pos_dev, int64_t pos, void* records,
                           void* tiles, uint64_t cap_tokens, void* stream);
+/* Decode step, K and V together: encode k and v (device [n_streams][dim]) and
+ * write them at token pos of every stream (as oq_cache_append).  For d = 128
+ * without QJL this is ONE kernel launch (each warp encodes its stream's
+ * vector exactly into shared memory and writes it into the tile); QJL keys
+ * take oq_cache_append per role.  k_records / v_records: optional device
+ * outputs for the OCTO records (NULL: not written). */
+oq_status oq_cache_append_kv(const oq_codec* ck, const oq_codec* cv, const void* k, const void* v,
+                             int dtype, uint64_t n_streams, const int64_t* pos_dev, int64_t pos,
+                             void* k_records, void* v_records, void* ktiles, void* vtiles,
+                             uint64_t cap_tokens, void* stream);
 size_t oq_cache_tile_bytes(const oq_codec* codec, int role); /* bytes per 32-token tile */
 size_t oq_cache_bytes(const oq_codec* codec, int role, uint64_t tokens); /* per stream */
 /* records: device [n_streams][rec_stride_tokens] records of n_tokens each

@@ -102,6 +102,8 @@ def lib():
         "oq_nccl_comm_destroy": ([vp], i32),
         "oq_cache_append": ([vp, i32, vp, i32, C.c_uint64, vp, C.c_int64, vp, vp, C.c_uint64, vp],
                             i32),
+        "oq_cache_append_kv": ([vp, vp, vp, vp, i32, C.c_uint64, vp, C.c_int64, vp, vp, vp, vp,
+                                C.c_uint64, vp], i32),
         "oq_decode": ([vp, vp, sz, vp, vp], i32),
         "oq_wire_header": ([cfgp, u64, C.c_char_p], i32),
         "oq_wire_parse_header": ([C.c_char_p, sz, cfgp, C.POINTER(u64)], i32),
@@ -401,26 +403,33 @@ class KVCache:
                                    _ptr(self.v), self.cap, _stream(stream)))
         self.tokens = n_tokens
 
-    def append(self, k, v, pos=None, stream=None):
+    def append(self, k, v, pos=None, stream=None, records=None):
         """Decode step: compress one new key and value per stream (k, v: CUDA
         [B, Hkv, dim]) and write them at token ``pos`` (an int, or a CUDA int64
-        tensor [B*Hkv] of per-stream positions; default: ``self.tokens``)."""
+        tensor [B*Hkv] of per-stream positions; default: ``self.tokens``).
+        K and V go through ONE fused launch (``oq_cache_append_kv``).
+        records: optional (k_records, v_records) uint8 CUDA tensors
+        [B*Hkv, record_bytes] that also receive the OCTO records."""
         import torch
         n = self.B * self.Hkv
         p = self.tokens if pos is None else pos
         L = lib()
-        for enc, x, tiles, role in ((self.enc_k, k, self.k, ROLE_K), (self.enc_v, v, self.v, ROLE_V)):
-            x = x.contiguous().reshape(n, enc.cfg.dim)
-            dt = _DTYPES.get(str(x.dtype).replace("torch.", ""))
-            if dt is None:
-                raise ValueError(f"unsupported dtype {x.dtype}")
-            recs = torch.empty((n, enc.record_bytes), dtype=torch.uint8, device=x.device)
-            if isinstance(p, int):
-                pd, ps = None, p
-            else:
-                pd, ps = _ptr(p.contiguous().to(torch.int64)), 0
-            _check(L.oq_cache_append(enc.handle, role, _ptr(x), dt, n, pd, ps, _ptr(recs),
-                                     _ptr(tiles), self.cap, _stream(stream)))
+        k = k.contiguous().reshape(n, self.enc_k.cfg.dim)
+        v = v.contiguous().reshape(n, self.enc_v.cfg.dim)
+        if v.dtype != k.dtype:
+            v = v.to(k.dtype)
+        dt = _DTYPES.get(str(k.dtype).replace("torch.", ""))
+        if dt is None:
+            raise ValueError(f"unsupported dtype {k.dtype}")
+        if isinstance(p, int):
+            pd, ps = None, p
+        else:
+            pos_t = p.contiguous().to(torch.int64)
+            pd, ps = _ptr(pos_t), 0
+        rk, rv = (None, None) if records is None else (_ptr(records[0]), _ptr(records[1]))
+        _check(L.oq_cache_append_kv(self.enc_k.handle, self.enc_v.handle, _ptr(k), _ptr(v), dt, n,
+                                    pd, ps, rk, rv, _ptr(self.k), _ptr(self.v), self.cap,
+                                    _stream(stream)))
         if isinstance(p, int):
             self.tokens = max(self.tokens, p + 1)
 

@@ -29,6 +29,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "encode_exact.cuh"
 
 namespace oqd {
 
@@ -952,6 +953,20 @@ __device__ __forceinline__ uint32_t rec_joint(const OqCodecParams& p, const uint
   return a | (b << p.b_dir) | (n << (2 * p.b_dir));
 }
 
+// The same joint code from a record held as 32-bit words (bits LSB-first):
+// the direction pair field is ixi | ieta << b_dir already.
+__device__ __forceinline__ uint32_t rec_field_w(const uint32_t* w, int pos, int bits) {
+  const int i = pos >> 5, sh = pos & 31;
+  const uint32_t v = sh + bits > 32 ? __funnelshift_r(w[i], w[i + 1], sh) : w[i] >> sh;
+  return v & ((1u << bits) - 1u);
+}
+__device__ __forceinline__ uint32_t rec_joint_w(const OqCodecParams& p, const uint32_t* w, int t) {
+  if (t >= kNT) return 0u;
+  const uint32_t d = rec_field_w(w, 32 + 2 * p.b_dir * t, 2 * p.b_dir);
+  const uint32_t n = rec_field_w(w, 32 + 8 * (int)p.dir_bytes + p.b_nrm * t, p.b_nrm);
+  return d | (n << (2 * p.b_dir));
+}
+
 __global__ void pack_tiles_kernel(OqCodecParams p, int role, const uint8_t* __restrict__ recs,
                                   size_t n_streams, size_t n_tok, size_t rec_stride,
                                   uint8_t* __restrict__ tiles, size_t tiles_cap) {
@@ -1033,49 +1048,71 @@ __global__ void pack_tiles_kernel(OqCodecParams p, int role, const uint8_t* __re
 // 31 tokens of the tile untouched (read-modify-write of the W-bit fields in
 // the lane runs).  One warp per stream; only the lanes owning that token's
 // slots write.  Same bit layout as pack_tiles_kernel.
-__global__ void __launch_bounds__(256) append_token_kernel(
-    OqCodecParams p, int role, const uint8_t* __restrict__ recs, size_t n_streams,
-    const int64_t* __restrict__ pos_dev, int64_t pos_scalar, uint8_t* __restrict__ tiles,
-    size_t tiles_cap) {
-  // per warp: the stream's record, and each writing lane's run words, staged
-  // in shared memory so that the read-modify-writes of the W-bit fields cost
-  // one batch of global loads and one of stores instead of a round trip each
-  __shared__ uint32_t rec_s[8][32];
-  __shared__ uint32_t run_s[8][32][21];
+// Write the record in rec (32 shared words, already complete) into token
+// slot pos of stream s's tile.  run: 32 x 21 words of warp-private shared
+// scratch.  Called by the whole warp; only the lanes owning the token's
+// slots touch the code runs.
+// Geometry of the append of token pos: the tile, and which lanes write.
+struct AppendGeo {
+  uint8_t* out;
+  int tt, nw;
+  bool writer;
+};
+__device__ __forceinline__ bool append_geo(const OqCodecParams& p, int role, size_t s, int64_t pos,
+                                           uint8_t* tiles, size_t tiles_cap, int lane,
+                                           AppendGeo& a) {
   const int W = 2 * p.b_dir + p.b_nrm;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const size_t s = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
-  if (s >= n_streams) return;
-  const int64_t pos = pos_dev ? pos_dev[s] : pos_scalar;
+  if (pos < 0 || (size_t)pos >= tiles_cap * 32) return false;
+  const int tb = role == 0 ? ktile_bytes(W, p.qjl) : vtile_bytes(W);
+  a.out = tiles + (s * tiles_cap + (size_t)pos / 32) * (size_t)tb;
+  a.tt = (int)(pos % 32);
+  const int g = lane >> 2, c = lane & 3;
+  a.writer = role == 0 ? (g == (a.tt & 7)) : (c == ((a.tt & 7) >> 1));
+  a.nw = role == 0 ? (c < 3 ? kw_full(W) : kw_3(W)) : (g < 7 ? vw_full(W) : vw_7(W));
+  return true;
+}
+
+// Start the asynchronous copy (cp.async, no register staging) of the writing
+// lanes' run words into run_w, so that it overlaps the key's encoding; the
+// caller waits (cp.async.wait_all) before append_record(staged = true).
+__device__ __forceinline__ void append_stage_runs(const OqCodecParams& p, int role, size_t s,
+                                                  int64_t pos, uint8_t* tiles, size_t tiles_cap,
+                                                  uint32_t (*run_w)[21], int lane) {
+  AppendGeo a;
+  if (!append_geo(p, role, s, pos, tiles, tiles_cap, lane, a) || !a.writer) return;
+  const int W = 2 * p.b_dir + p.b_nrm;
+  const uint32_t* codes = reinterpret_cast<const uint32_t*>(a.out + 128);
+  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(run_w[lane]);
+  for (int i = 0; i < a.nw; ++i) {
+    const uint32_t* src = codes + (role == 0 ? k_word_off(W, lane, i) : v_word_off(W, lane, i));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 4 * i), "l"(src));
+  }
+}
+
+__device__ __forceinline__ void append_record(const OqCodecParams& p, int role, const uint32_t* rec,
+                                              uint32_t (*run_w)[21], size_t s, int64_t pos,
+                                              uint8_t* __restrict__ tiles, size_t tiles_cap,
+                                              int lane, bool staged = false) {
+  const int W = 2 * p.b_dir + p.b_nrm;
   if (pos < 0 || (size_t)pos >= tiles_cap * 32) return;
   const size_t tile = (size_t)pos / 32;
   const int tt = (int)(pos % 32);
   const int tb = role == 0 ? ktile_bytes(W, p.qjl) : vtile_bytes(W);
   uint8_t* out = tiles + (s * tiles_cap + tile) * (size_t)tb;
-  {
-    const uint8_t* rg = recs + s * p.rec_bytes;
-    uint32_t w = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t bi = 4 * lane + i;
-      if (bi < p.rec_bytes) w |= (uint32_t)rg[bi] << (8 * i);
-    }
-    rec_s[wib][lane] = w;
-  }
-  __syncwarp();
-  const uint8_t* r = reinterpret_cast<const uint8_t*>(rec_s[wib]);
+  const uint8_t* r = reinterpret_cast<const uint8_t*>(rec);
   const int g = lane >> 2, c = lane & 3;
   const int tg = tt & 7, tk = tt >> 3;  // token = g + 8k in the K map and the gamma slots
-  if (lane == 0)
-    reinterpret_cast<float*>(out)[tg * 4 + tk] = __uint_as_float(rec_s[wib][0]);
+  if (lane == 0) reinterpret_cast<float*>(out)[tg * 4 + tk] = __uint_as_float(rec[0]);
   uint32_t* codes = reinterpret_cast<uint32_t*>(out + 128);
   const bool writer = role == 0 ? (g == tg) : (c == ((tt & 7) >> 1));
   if (!writer) return;
   const int nw = role == 0 ? (c < 3 ? kw_full(W) : kw_3(W)) : (g < 7 ? vw_full(W) : vw_7(W));
-  uint32_t* run = run_s[wib][lane];
+  uint32_t* run = run_w[lane];
   auto woff = [&](int i) { return role == 0 ? k_word_off(W, lane, i) : v_word_off(W, lane, i); };
+  if (!staged) {
 #pragma unroll 4
-  for (int i = 0; i < nw; ++i) run[i] = codes[woff(i)];
+    for (int i = 0; i < nw; ++i) run[i] = codes[woff(i)];
+  }
   const int FW = fw(W);
   const uint32_t m = (1u << FW) - 1u;
   auto put = [&](int slot, uint32_t code) {
@@ -1088,7 +1125,7 @@ __global__ void __launch_bounds__(256) append_token_kernel(
   };
   if (role == 0) {
     const int nu = c < 3 ? 11 : 10;
-    for (int u = 0; u < nu; ++u) put(u * 4 + tk, rec_joint(p, r, 11 * c + u));
+    for (int u = 0; u < nu; ++u) put(u * 4 + tk, rec_joint_w(p, rec, 11 * c + u));
     if (p.qjl) {
       uint8_t* qa = out + 128 + 4 * kcode_words(W);
       const int sign_off = 4 + p.dir_bytes + p.nrm_bytes + 2;
@@ -1103,10 +1140,103 @@ __global__ void __launch_bounds__(256) append_token_kernel(
     // V map: token v_token(c, k) = 16 (k >> 2) + 2c + (k & 1) + 8 ((k >> 1) & 1)
     const int k = (tt >> 4) * 4 + ((tt >> 3) & 1) * 2 + (tt & 1);
     const int nu = g < 7 ? 6 : 1;
-    for (int u = 0; u < nu; ++u) put(u * 8 + k, rec_joint(p, r, 6 * g + u));
+    for (int u = 0; u < nu; ++u) put(u * 8 + k, rec_joint_w(p, rec, 6 * g + u));
   }
 #pragma unroll 4
   for (int i = 0; i < nw; ++i) codes[woff(i)] = run[i];
+}
+
+// Decode-step append (oq_cache_append): write ONE token per stream — the
+// record rec[s] — into token slot pos of the stream's tile, leaving the other
+// 31 tokens of the tile untouched (read-modify-write of the W-bit fields in
+// the lane runs).  One warp per stream.  Same bit layout as pack_tiles_kernel.
+// The record and each writing lane's run words are staged in shared memory so
+// the read-modify-writes cost one batch of global loads and one of stores.
+__global__ void __launch_bounds__(256) append_token_kernel(
+    OqCodecParams p, int role, const uint8_t* __restrict__ recs, size_t n_streams,
+    const int64_t* __restrict__ pos_dev, int64_t pos_scalar, uint8_t* __restrict__ tiles,
+    size_t tiles_cap) {
+  __shared__ uint32_t rec_s[8][32];
+  __shared__ uint32_t run_s[8][32][21];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const size_t s = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+  if (s >= n_streams) return;
+  const int64_t pos = pos_dev ? pos_dev[s] : pos_scalar;
+  {
+    const uint8_t* rg = recs + s * p.rec_bytes;
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t bi = 4 * lane + i;
+      if (bi < p.rec_bytes) w |= (uint32_t)rg[bi] << (8 * i);
+    }
+    rec_s[wib][lane] = w;
+  }
+  __syncwarp();
+  append_record(p, role, rec_s[wib], run_s[wib], s, pos, tiles, tiles_cap, lane);
+}
+
+// Fused decode-step append of K AND V (oq_cache_append_kv): blockIdx.y is the
+// role; each warp encodes its stream's new vector (encode_key_warp, exact)
+// straight into shared memory and writes it into the tile — one launch per
+// step instead of compress + append for each of K and V.  d = 128, no QJL.
+constexpr int kAppendWarps = 4;
+__global__ void __launch_bounds__(32 * kAppendWarps) append_fused_kernel(
+    const __grid_constant__ OqCodecParams pk, const __grid_constant__ OqCodecParams pv,
+    const void* __restrict__ xk, const void* __restrict__ xv, int dtype, size_t n_streams,
+    const int64_t* __restrict__ pos_dev, int64_t pos_scalar, uint8_t* __restrict__ rk,
+    uint8_t* __restrict__ rv, uint8_t* __restrict__ tk, uint8_t* __restrict__ tv,
+    size_t tiles_cap) {
+  __shared__ double row_s[kAppendWarps][132];
+  __shared__ uint32_t rec_s[kAppendWarps][32];
+  __shared__ uint32_t run_s[kAppendWarps][32][21];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, role = blockIdx.y;
+  const size_t s = blockIdx.x * (size_t)kAppendWarps + wib;
+  if (s >= n_streams) return;
+  const OqCodecParams& p = role ? pv : pk;
+  const int64_t pos = pos_dev ? pos_dev[s] : pos_scalar;
+  uint8_t* tiles = role ? tv : tk;
+  {
+    // warm L1 with the codebook tables joint_round reads (their dependent
+    // lookups would otherwise each pay an L2 round trip) while the key is
+    // loaded and rotated; the tile's run words are copied asynchronously
+    const uint32_t kk = p.K * p.K;
+    const int t = threadIdx.x;
+    auto pf = [](const void* a) { asm volatile("prefetch.global.L1 [%0];" ::"l"(a)); };
+    for (uint32_t i = t; i < kk * 16 / 128; i += blockDim.x) pf(reinterpret_cast<const uint8_t*>(p.dirs32) + 128 * i);
+    for (uint32_t i = t; i < kk * 24 / 128; i += blockDim.x) pf(reinterpret_cast<const uint8_t*>(p.dirs64) + 128 * i);
+    for (int i = t; i < 32; i += blockDim.x) {
+      pf(reinterpret_cast<const uint8_t*>(p.xi_lut) + 128 * i);
+      pf(reinterpret_cast<const uint8_t*>(p.rho_lut) + 128 * i);
+    }
+    if (t == 0) {
+      pf(p.xi_bnd);
+      pf(p.rho_bnd);
+      pf(p.rho_c);
+    }
+  }
+  append_stage_runs(p, role, s, pos, tiles, tiles_cap, run_s[wib], lane);
+  encode_key_warp(p, role ? xv : xk, dtype, s, row_s[wib], rec_s[wib], lane);
+  uint8_t* recs = role ? rv : rk;
+  if (recs) {
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(rec_s[wib]);
+    for (uint32_t b = lane; b < p.rec_bytes; b += 32) recs[s * p.rec_bytes + b] = src[b];
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+  append_record(p, role, rec_s[wib], run_s[wib], s, pos, tiles, tiles_cap, lane, true);
+}
+
+cudaError_t launch_append_fused(const OqCodecParams& pk, const OqCodecParams& pv, const void* xk,
+                                const void* xv, int dtype, size_t n_streams,
+                                const int64_t* pos_dev, int64_t pos_scalar, uint8_t* rk,
+                                uint8_t* rv, uint8_t* tk, uint8_t* tv, size_t tiles_cap,
+                                cudaStream_t st) {
+  if (n_streams == 0) return cudaSuccess;
+  const dim3 grid((unsigned)((n_streams + kAppendWarps - 1) / kAppendWarps), 2);
+  append_fused_kernel<<<grid, 32 * kAppendWarps, 0, st>>>(pk, pv, xk, xv, dtype, n_streams, pos_dev,
+                                                         pos_scalar, rk, rv, tk, tv, tiles_cap);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_append_token(const OqCodecParams& p, int role, const uint8_t* recs,

@@ -477,6 +477,49 @@ oq_status oq_cache_append(const oq_codec* c, int role, const void* x, int dtype,
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "append kernel");
 }
 
+oq_status oq_cache_append_kv(const oq_codec* ck, const oq_codec* cv, const void* k, const void* v,
+                             int dtype, uint64_t n_streams, const int64_t* pos_dev, int64_t pos,
+                             void* k_records, void* v_records, void* ktiles, void* vtiles,
+                             uint64_t cap_tokens, void* stream) {
+  oq_status s = check_codec(ck);
+  if (!s) s = check_codec(cv);
+  if (s) return s;
+  if (n_streams && (!k || !v || !ktiles || !vtiles))
+    return fail(OQ_ERR_INVALID_ARGUMENT, "null buffer");
+  if (!pos_dev && (pos < 0 || (uint64_t)pos >= cap_tokens))
+    return fail(OQ_ERR_INVALID_ARGUMENT, "append position outside the cache");
+  if (oqd::attention_tile_bytes(ck->p, OQ_ROLE_K) == 0 ||
+      oqd::attention_tile_bytes(cv->p, OQ_ROLE_V) == 0)
+    return fail(OQ_ERR_UNSUPPORTED, "attention tile format needs dim 128 and 2*b_dir+b_nrm <= 13");
+  if (cv->cfg.qjl) return fail(OQ_ERR_INVALID_ARGUMENT, "the V codec carries no QJL sidecar");
+  if (dtype != OQ_F32 && dtype != OQ_F64 && dtype != OQ_F16 && dtype != OQ_BF16)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "bad dtype");
+  if (n_streams == 0) return OQ_OK;
+  cudaStream_t st = as_stream(stream);
+  if (!ck->cfg.qjl) {  // one launch: both roles encoded and written in place
+    cudaError_t e = oqd::launch_append_fused(
+        ck->p, cv->p, k, v, dtype, n_streams, pos_dev, pos, static_cast<uint8_t*>(k_records),
+        static_cast<uint8_t*>(v_records), static_cast<uint8_t*>(ktiles),
+        static_cast<uint8_t*>(vtiles), (cap_tokens + 31) / 32, st);
+    return e == cudaSuccess ? OQ_OK : cuda_fail(e, "fused append kernel");
+  }
+  // QJL keys: compress + append per role, through record scratch if needed
+  void* scratch = nullptr;
+  const size_t rbk = ck->p.rec_bytes, rbv = cv->p.rec_bytes;
+  if (!k_records || !v_records) {
+    cudaError_t e = cudaMallocAsync(&scratch, n_streams * (rbk + rbv), st);
+    if (e != cudaSuccess) return cuda_fail(e, "append scratch");
+  }
+  uint8_t* sk = static_cast<uint8_t*>(scratch);
+  s = oq_cache_append(ck, OQ_ROLE_K, k, dtype, n_streams, pos_dev, pos,
+                      k_records ? k_records : sk, ktiles, cap_tokens, stream);
+  if (!s)
+    s = oq_cache_append(cv, OQ_ROLE_V, v, dtype, n_streams, pos_dev, pos,
+                        v_records ? v_records : sk + n_streams * rbk, vtiles, cap_tokens, stream);
+  if (scratch) cudaFreeAsync(scratch, st);
+  return s;
+}
+
 static int parts_per_row(const oq_codec* ck, const oq_attn_shape* sh, uint64_t t0, uint64_t t1,
                          int n_splits) {
   return oqd::attention_num_parts(sh->B, sh->Hq, sh->Hkv, sh->T, t0, t1, n_splits, ck->num_sms);

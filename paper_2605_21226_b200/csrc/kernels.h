@@ -64,6 +64,12 @@ cudaError_t launch_pack_tiles(const OqCodecParams& p, int role, const uint8_t* r
 cudaError_t launch_append_token(const OqCodecParams& p, int role, const uint8_t* recs,
                                 size_t n_streams, const int64_t* pos_dev, int64_t pos_scalar,
                                 uint8_t* tiles, size_t tiles_cap, cudaStream_t st);
+// fused decode-step append of K and V (d = 128, no QJL): encode + tile write
+cudaError_t launch_append_fused(const OqCodecParams& pk, const OqCodecParams& pv, const void* xk,
+                                const void* xv, int dtype, size_t n_streams,
+                                const int64_t* pos_dev, int64_t pos_scalar, uint8_t* rk,
+                                uint8_t* rv, uint8_t* tk, uint8_t* tv, size_t tiles_cap,
+                                cudaStream_t st);
 // K5: query prep -> mma fragments (a.qfrag)
 cudaError_t launch_qprep(const OqCodecParams& pk, const AttnArgs& a, cudaStream_t st);
 // K3: split-K partials over [t_begin, t_end)

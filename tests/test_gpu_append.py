@@ -70,3 +70,37 @@ def test_append_ragged_positions(cuda):
         per_k, per_v = (cap + 31) // 32 * kt, (cap + 31) // 32 * vt
         assert torch.equal(app.k[b * per_k:b * per_k + ntile * kt], one.k[:ntile * kt]), b
         assert torch.equal(app.v[b * per_v:b * per_v + ntile * vt], one.v[:ntile * vt]), b
+
+
+@pytest.mark.parametrize("qjl", [False, True])
+def test_append_records_and_bf16(cuda, qjl):
+    """The fused K+V append (one launch without QJL) hands back the same OCTO
+    records as oq_compress on bf16 inputs, and writes the same tiles as pack."""
+    import torch
+    B, Hkv, cap = 4, 8, 64
+    n = B * Hkv
+    ek, ev = _encoders(3, qjl)
+    g = torch.Generator(device=cuda).manual_seed(11)
+    k = torch.randn((B, Hkv, 128), device=cuda, generator=g).to(torch.bfloat16)
+    v = torch.randn((B, Hkv, 128), device=cuda, generator=g).to(torch.bfloat16)
+    rk = torch.zeros((n, ek.record_bytes), dtype=torch.uint8, device=cuda)
+    rv = torch.zeros((n, ev.record_bytes), dtype=torch.uint8, device=cuda)
+    app = oq.KVCache(ek, ev, B, Hkv, cap)
+    app.append(k, v, pos=37, records=(rk, rv))
+    wk, wv = ek.compress(k.reshape(n, 128)), ev.compress(v.reshape(n, 128))
+    assert torch.equal(rk, wk) and torch.equal(rv, wv)
+    ref = oq.KVCache(ek, ev, B, Hkv, cap)
+    z = lambda r: torch.zeros((n, 38, r.shape[1]), dtype=torch.uint8, device=cuda)
+    zk, zv = z(wk), z(wv)
+    zk[:, 37], zv[:, 37] = wk, wv
+    # tokens 0..36 of `ref` are all-zero records; append leaves app's untouched
+    # (zero-initialised tiles), so only token 37's fields can differ
+    ref.pack(zk, zv, 38)
+    kt, vt = ek.tile_bytes(0), ev.tile_bytes(1)
+    per_k, per_v = (cap + 31) // 32 * kt, (cap + 31) // 32 * vt
+    for s in range(n):
+        a = app.k[s * per_k + kt:s * per_k + 2 * kt]
+        b = ref.k[s * per_k + kt:s * per_k + 2 * kt]
+        assert torch.equal(a, b), s
+        assert torch.equal(app.v[s * per_v + vt:s * per_v + 2 * vt],
+                           ref.v[s * per_v + vt:s * per_v + 2 * vt]), s
