@@ -384,8 +384,9 @@ def main():
         torch.cuda.synchronize()
         ap = a0.elapsed_time(a1) / args.steps
         st = a1.elapsed_time(a2) / args.steps
-        step_info = {"what": "decoder step: bf16 K/V of B*Hkv streams appended (K1 + tile insert, "
-                             "per role) then decode attention over the 128K-token cache",
+        step_info = {"what": "decoder step: bf16 K/V of B*Hkv streams appended (one fused exact "
+                             "encode + tile insert launch for K and V) then decode attention over "
+                             "the 128K-token cache",
                      "append_us": ap * 1e3, "append_plus_attention_us": st * 1e3}
         # the same step captured once in a CUDA graph and replayed (how a serving
         # loop removes the per-launch host overhead of the small append kernels)

@@ -42,7 +42,11 @@ def main():
            f"({tr[att] / r['algorithmic_bytes_per_launch']:.3f}x)",
            f"- e2e (pinned q in, out back, public API): {d['e2e']['value']:.0f} GB/s",
            f"- CPU reference (oracle/_ref, {d['cpu_baseline']['cores']} host threads): "
-           f"{d['cpu_baseline']['value']:.3f} GB/s\n",
+           f"{d['cpu_baseline']['value']:.3f} GB/s",
+           (f"- decoder step (append K+V of 32 streams + attention): append "
+            f"{d['decode_step']['append_us']:.1f} µs, step {d['decode_step']['append_plus_attention_us']:.1f} µs"
+            f" eager / {d['decode_step'].get('graph_append_plus_attention_us', float('nan')):.1f} µs "
+            f"CUDA graph\n" if d.get("decode_step") else "\n"),
            "| bits | K1 compress µs | G keys/s | GB/s (% HBM) | flagged keys | K2 decode µs | GB/s (% HBM) |",
            "|---|---|---|---|---|---|---|"]
     for b, v in c["sweep_bits"].items():
