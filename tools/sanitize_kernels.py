@@ -13,6 +13,7 @@ for bits in (2, 3, 4):
         x = torch.randn((3000, 128), device=dev, generator=g)   # partial tail blocks too
         r = enc.compress(x)
         enc.decode(r)
+        enc.compress(x[:77].to(torch.bfloat16))  # one-warp-per-key small-batch encoder
 B, Hkv, T = 2, 2, 300
 bd, bn = oq.default_bit_split(3)
 ek = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=5))
@@ -22,6 +23,17 @@ v = torch.randn((B * Hkv * T, 128), device=dev, generator=g)
 cache = oq.KVCache(ek, ev, B, Hkv, T + 40)
 cache.pack(ek.compress(k), ev.compress(v), T)
 cache.append(torch.randn((B, Hkv, 128), device=dev), torch.randn((B, Hkv, 128), device=dev))
+# fused K+V append with per-stream positions and record outputs, bf16 inputs
+rk = torch.empty((B * Hkv, ek.record_bytes), dtype=torch.uint8, device=dev)
+rv = torch.empty((B * Hkv, ev.record_bytes), dtype=torch.uint8, device=dev)
+cache.append(torch.randn((B, Hkv, 128), device=dev).to(torch.bfloat16),
+             torch.randn((B, Hkv, 128), device=dev).to(torch.bfloat16),
+             pos=torch.arange(B * Hkv, device=dev) + T, records=(rk, rv))
+# QJL keys: compress + insert per role
+eq = oq.Encoder(oq.CodecConfig(b_dir=3, b_nrm=1, qjl=True, rotation_seed=7))
+ev2 = oq.Encoder(oq.CodecConfig(b_dir=3, b_nrm=1, rotation_seed=8))
+c2 = oq.KVCache(eq, ev2, B, Hkv, 64)
+c2.append(torch.randn((B, Hkv, 128), device=dev), torch.randn((B, Hkv, 128), device=dev), pos=3)
 q = torch.randn((B, 7 * Hkv, 128), device=dev, generator=g)
 oq.attention_decode(q, cache)
 oq.attention_partials(q, cache, 0, cache.tokens)
