@@ -342,6 +342,126 @@ __global__ void __launch_bounds__(32 * kSmallWarps) compress_small_kernel(
   for (uint32_t b = lane; b < rb; b += 32) dst[b] = src[b];
 }
 
+// ---------------------------------------------------------------------------
+// Exact fixup of the certified fp32 pass (compress_fast.cu).  Per round a CTA
+// takes 16 warps x kFixKeys flagged keys: each warp recomputes its keys'
+// reference fp64 rotated coordinates from the stored exact inv
+// (rotate_key_warp) and queues the flagged triplets (3 doubles + key + t) in
+// shared memory; then every thread re-rounds one queued triplet exactly
+// (joint_round: a long dependent chain, so the triplets of many keys run
+// side by side instead of one lane per key) and patches its direction-pair
+// and norm fields into the record in place — the pass masks every field to
+// its width, so the other fields are already final.  Records of different
+// keys may share a 32-bit word, hence atomic clear + set on disjoint bits.
+constexpr int kFixWarps = 16, kFixKeys = 4, kFixQ = 896;
+
+struct FixTriplet {
+  double t0, t1, t2;
+  uint32_t key, t;
+};
+
+__device__ __forceinline__ void patch_field(uint32_t* words, size_t pos, int bits, uint32_t v) {
+  const size_t w = pos >> 5;
+  const int sh = (int)(pos & 31);
+  const uint32_t m = (1u << bits) - 1u;
+  atomicAnd(&words[w], ~(m << sh));
+  atomicOr(&words[w], (v & m) << sh);
+  if (sh + bits > 32) {
+    const int hi = sh + bits - 32;
+    atomicAnd(&words[w + 1], ~((1u << hi) - 1u));
+    atomicOr(&words[w + 1], (v & m) >> (bits - hi));
+  }
+}
+
+__device__ __forceinline__ void fix_triplet(const OqCodecParams& p, const CompressSmem& tabs,
+                                            const float4* d32, uint32_t* words, const FixTriplet& q) {
+  const uint32_t code = joint_round(p, tabs, d32, q.t0, q.t1, q.t2);
+  const uint32_t pr = (code & 0xff) | (((code >> 8) & 0xff) << p.b_dir), ir = code >> 16;
+  const size_t base = (size_t)8 * q.key * p.rec_bytes;
+  const int pb = 2 * p.b_dir, nb = p.b_nrm;
+  patch_field(words, base + 32 + (size_t)pb * q.t, pb, pr);
+  patch_field(words, base + 32 + 8 * (size_t)p.dir_bytes + (size_t)nb * q.t, nb, ir);
+}
+
+__global__ void __launch_bounds__(32 * kFixWarps, 1) compress_fixup_kernel(
+    OqCodecParams p, const void* __restrict__ x, int dtype, uint8_t* __restrict__ out,
+    const FlagEntry* __restrict__ flags, const uint32_t* __restrict__ flag_cnt) {
+  __shared__ double row_s[kFixWarps][132];
+  __shared__ FixTriplet queue[kFixQ];
+  __shared__ uint32_t qn;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t n = *flag_cnt;
+  {
+    // warm this SM's L1 with the codebook tables: joint_round's lookups form
+    // a dependent chain that would otherwise pay an L2 round trip per step
+    const uint32_t kk = p.K * p.K;
+    auto pf = [](const void* a) { asm volatile("prefetch.global.L1 [%0];" ::"l"(a)); };
+    for (uint32_t l = threadIdx.x; l < (kk * 16 + 127) / 128; l += blockDim.x)
+      pf(reinterpret_cast<const uint8_t*>(p.dirs32) + 128 * l);
+    for (uint32_t l = threadIdx.x; l < (kk * 24 + 127) / 128; l += blockDim.x)
+      pf(reinterpret_cast<const uint8_t*>(p.dirs64) + 128 * l);
+    for (uint32_t l = threadIdx.x; l < 32; l += blockDim.x) {
+      pf(reinterpret_cast<const uint8_t*>(p.xi_lut) + 128 * l);
+      pf(reinterpret_cast<const uint8_t*>(p.rho_lut) + 128 * l);
+    }
+    if (threadIdx.x == 0) {
+      pf(p.xi_bnd);
+      pf(p.rho_bnd);
+      pf(p.rho_c);
+      qn = 0;
+    }
+  }
+  __syncthreads();
+  const CompressSmem tabs = global_tables(p);
+  const float4* d32 = reinterpret_cast<const float4*>(p.dirs32);
+  uint32_t* words = reinterpret_cast<uint32_t*>(out);
+  constexpr size_t PER_CTA = (size_t)kFixWarps * kFixKeys;
+  for (size_t e0 = blockIdx.x * PER_CTA; e0 < n; e0 += (size_t)gridDim.x * PER_CTA) {
+    // ---- rotations: this warp's keys, all rows requested up front ----------
+    const size_t w0 = e0 + (size_t)wib * kFixKeys;
+    FlagEntry f[kFixKeys];
+    double k[kFixKeys][4];
+#pragma unroll
+    for (int j = 0; j < kFixKeys; ++j)
+      if (w0 + j < n) f[j] = flags[w0 + j];
+#pragma unroll
+    for (int j = 0; j < kFixKeys; ++j)
+      if (w0 + j < n)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          k[j][i] = load_as_double(x, dtype, (size_t)f[j].key * 128 + 4 * lane + i);
+#pragma unroll
+    for (int j = 0; j < kFixKeys; ++j) {
+      if (w0 + j >= n) break;
+      rotate_key_warp(p, k[j], f[j].inv, row_s[wib], lane);
+      const double* row = row_s[wib];
+      for (int t = lane; t < 43; t += 32) {
+        if (!(((t < 32 ? f[j].mlo >> t : f[j].mhi >> (t - 32))) & 1u)) continue;
+        const FixTriplet q{row[3 * t], row[3 * t + 1], row[3 * t + 2], f[j].key, (uint32_t)t};
+        const uint32_t slot = atomicAdd(&qn, 1u);
+        if (slot < kFixQ) queue[slot] = q;
+        else fix_triplet(p, tabs, d32, words, q);  // queue full: decide it here
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // ---- decisions: one queued triplet per thread -------------------------
+    const uint32_t m = min(qn, (uint32_t)kFixQ);
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) fix_triplet(p, tabs, d32, words, queue[i]);
+    __syncthreads();
+    if (threadIdx.x == 0) qn = 0;
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_compress_fixup(const OqCodecParams& p, const void* x, int dtype, uint8_t* out,
+                                  const FlagEntry* flags, const uint32_t* flag_cnt,
+                                  cudaStream_t st, int num_sms) {
+  // the count lives on the device: a fixed persistent grid strides over it
+  compress_fixup_kernel<<<num_sms, 32 * kFixWarps, 0, st>>>(p, x, dtype, out, flags, flag_cnt);
+  return cudaGetLastError();
+}
+
 template <int D>
 static size_t compress_smem(const OqCodecParams& p) {
   using S = CompressShape<D>;
@@ -422,16 +542,15 @@ cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, si
     return e;
   }
   if (impl == 1 && compress_fast_ok(p, dtype, x, out)) {
-    // certified fp32 pass, then the exact two-lanes-per-key kernel over the
-    // keys it flagged
+    // certified fp32 pass, then the exact re-rounding of the triplets it
+    // could not decide
     uint32_t* ws = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), (n + 4) * sizeof(uint32_t), st);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), 32 + n * sizeof(FlagEntry), st);
     if (e != cudaSuccess) return e;
+    FlagEntry* fl = reinterpret_cast<FlagEntry*>(ws + 8);
     e = cudaMemsetAsync(ws, 0, sizeof(uint32_t), st);
-    if (e == cudaSuccess)
-      e = launch_compress_fast(p, x, dtype, n, out, ws + 4, ws, st, num_sms);
-    if (e == cudaSuccess)
-      e = launch_compress_x2(p, x, dtype, n, out, st, num_sms, ws + 4, ws);
+    if (e == cudaSuccess) e = launch_compress_fast(p, x, dtype, n, out, fl, ws, st, num_sms);
+    if (e == cudaSuccess) e = launch_compress_fixup(p, x, dtype, out, fl, ws, st, num_sms);
     if (e == cudaSuccess && flagged)
       e = cudaMemcpyAsync(flagged, ws, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
     const cudaError_t f = cudaFreeAsync(ws, st);

@@ -22,9 +22,12 @@
 //    the 3x3 argmax (codec.hpp:164-189) and the norm bucket — is taken in
 //    fp32 and CERTIFIED: it must clear its decision boundary by more than the
 //    propagated error bound, otherwise the key is flagged;
-//  * flagged keys are appended to a list and re-encoded afterwards by the
-//    exact fp64 kernel (compress.cu), so every record is bit-identical to the
-//    reference; the flagged count is reported.
+//  * a triplet whose decisions miss a margin is marked in the key's 43-bit
+//    mask; flagged keys (mask, exact fp64 inv) are appended to a list and
+//    only their marked triplets are re-rounded afterwards in exact fp64 and
+//    patched into the record (compress.cu, compress_fixup_kernel), so every
+//    record is bit-identical to the reference; the flagged key count is
+//    reported.
 //  * records are assembled in registers at compile-time bit positions,
 //    merged across lanes at shared word boundaries with one shuffle, and the
 //    warp's 32 records leave with one TMA bulk store.
@@ -84,7 +87,7 @@ __device__ __forceinline__ uint32_t cf_bucket(float x, float g, const float4* lu
 template <int BD, int BN, int MODE, int DT>
 __global__ void __launch_bounds__(kCFThreads, 1)
     compress_fast_kernel(OqCodecParams p, const void* __restrict__ x, size_t n,
-                         uint8_t* __restrict__ out, uint32_t* __restrict__ flag_idx,
+                         uint8_t* __restrict__ out, FlagEntry* __restrict__ flags,
                          uint32_t* __restrict__ flag_cnt) {
   using S = CFS<BD, BN>;
   constexpr int K = S::K;
@@ -190,7 +193,9 @@ __global__ void __launch_bounds__(kCFThreads, 1)
     const double inv = __ddiv_rn(1.0, gamma > 1e-12 ? gamma : 1e-12);
     const float c32 = (float)(inv * p.inv_sqrt_d);
     // outside [2^-60, 2^60] the fp32 rotation could lose range: exact path
-    bool ok = live && gamma > 8.7e-19 && gamma < 1.1e18;
+    // for every triplet
+    const bool ok = gamma > 8.7e-19 && gamma < 1.1e18;
+    uint64_t fmask = 0;  // triplets whose decisions missed their margins
 
     // ---- rotation in fp32: ur = H (s .* k) * c -------------------------------
 #pragma unroll
@@ -238,11 +243,13 @@ __global__ void __launch_bounds__(kCFThreads, 1)
         e[4] = v1.x; e[5] = v1.y; e[6] = v1.z; e[7] = v1.w;
         e[8] = v2.x; e[9] = v2.y; e[10] = v2.z; e[11] = v2.w;
       }
+      uint32_t gmask = 0;  // undecided triplets of this group of 4
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int t = 4 * q + j;
         if (t >= S::NT) break;
         const bool pad = t == S::NT - 1;  // elements 126, 127 and the zero pad
+        bool okt = true;
         const float t0 = e[3 * j], t1 = e[3 * j + 1], t2 = pad ? 0.f : e[3 * j + 2];
         const float a0 = fabsf(t0), a1 = fabsf(t1), a2 = fabsf(t2);
         const float l1 = a0 + a1 + a2;
@@ -256,11 +263,11 @@ __global__ void __launch_bounds__(kCFThreads, 1)
         // hemisphere and, below it, sgn(px), sgn(py) (octahedral.hpp:29-30):
         // |t_i| > E0 + 2.01u |t_i| is implied by |t_i| > 1.0001 E0
         const float es = 1.0001f * E0;
-        ok = ok && l1 > 1e-6f && (pad || a2 > es) && (up || (a0 > es && a1 > es));
+        okt = l1 > 1e-6f && (pad || a2 > es) && (up || (a0 > es && a1 > es));
         const float xi = up ? t0 * il : copysignf(1.f - a1 * il, t0);
         const float eta = up ? t1 * il : copysignf(1.f - a0 * il, t1);
-        const uint32_t sx = cf_bucket(xi, gx, mylut, ok);
-        const uint32_t sy = cf_bucket(eta, gx, mylut, ok);
+        const uint32_t sx = cf_bucket(xi, gx, mylut, okt);
+        const uint32_t sy = cf_bucket(eta, gx, mylut, okt);
         uint32_t ix = sx, iy = sy;
         float rv, gr;
         if (MODE == 0) {  // scalar: rho of clamp(|t|, 0, 1) (codec.hpp:154-162)
@@ -285,7 +292,7 @@ __global__ void __launch_bounds__(kCFThreads, 1)
           // score error: ||dt|| <= Et (rotation) + |t| u/2 (fp32 table) + 3u |t|
           // (dot rounding), with |t| <= l1
           const float gs = (E0 + 5.53f * U * l1) * 1.001f;
-          ok = ok && (b1 - b2 > 2.002f * gs);
+          okt = okt && (b1 - b2 > 2.002f * gs);
           ix = sx + (wi >> 2) - 1;
           iy = sy + (wi & 3) - 1;
           rv = b1;
@@ -296,10 +303,12 @@ __global__ void __launch_bounds__(kCFThreads, 1)
 #pragma unroll
         for (int i = 0; i < S::KR - 1; ++i) {
           ir += rv >= rbnd[i] ? 1u : 0u;
-          ok = ok && fabsf(rv - rbnd[i]) > gr + U;
+          okt = okt && fabsf(rv - rbnd[i]) > gr + U;
         }
-        // ---- append the fields ------------------------------------------------
-        dacc |= (uint64_t)(ix | (iy << BD)) << dn;
+        gmask |= (okt ? 0u : 1u) << j;
+        // ---- append the fields (masked to their widths: an undecided
+        // triplet's fields are patched in place by the exact fixup) ----------
+        dacc |= (uint64_t)((ix & (K - 1)) | ((iy & (K - 1)) << BD)) << dn;
         dn += 2 * BD;
         if (dn >= 32) {
           put(dw++, (uint32_t)dacc);
@@ -314,6 +323,7 @@ __global__ void __launch_bounds__(kCFThreads, 1)
           nn -= 32;
         }
       }
+      fmask |= (uint64_t)gmask << (4 * q);
     }
     if (dn > 0) put(dw, (uint32_t)dacc);
     if (nn > 0) put(nw, (uint32_t)nacc);
@@ -326,13 +336,23 @@ __global__ void __launch_bounds__(kCFThreads, 1)
 #pragma unroll
     for (int i = 0; i <= S::RW; ++i) w[i] = i < S::RW ? scr[32 * i] : 0u;
 
-    // ---- flagged keys: exact re-encode later --------------------------------
-    const uint32_t bad = __ballot_sync(kFull, live && !ok);
+    // ---- keys with undecided triplets: exact fixup later ---------------------
+    if (!ok) fmask = (1ull << S::NT) - 1;
+    const uint32_t bad = __ballot_sync(kFull, live && fmask != 0);
     if (bad) {
       uint32_t basei = 0;
       if (lane == 0) basei = atomicAdd(flag_cnt, (uint32_t)__popc(bad));
       basei = __shfl_sync(kFull, basei, 0);
-      if (live && !ok) flag_idx[basei + __popc(bad & ((1u << lane) - 1u))] = (uint32_t)(k0 + lane);
+      if (live && fmask != 0) {
+        FlagEntry fe;
+        fe.key = (uint32_t)(k0 + lane);
+        fe.mlo = (uint32_t)fmask;
+        fe.mhi = (uint32_t)(fmask >> 32);
+        fe.pad = 0;
+        fe.inv = inv;
+        fe.pad2 = 0.0;
+        flags[basei + __popc(bad & ((1u << lane) - 1u))] = fe;
+      }
     }
 
     // ---- the warp's 32 records -> shared buffer -> one bulk store ------------
@@ -378,7 +398,7 @@ __global__ void __launch_bounds__(kCFThreads, 1)
 
 template <int BD, int BN, int MODE, int DT>
 static cudaError_t launch_cf_t(const OqCodecParams& p, const void* x, size_t n, uint8_t* out,
-                               uint32_t* flag_idx, uint32_t* flag_cnt, cudaStream_t st,
+                               FlagEntry* flag_idx, uint32_t* flag_cnt, cudaStream_t st,
                                int num_sms) {
   using S = CFS<BD, BN>;
   cudaError_t e = set_smem_once(compress_fast_kernel<BD, BN, MODE, DT>, S::SMEM);
@@ -393,7 +413,7 @@ static cudaError_t launch_cf_t(const OqCodecParams& p, const void* x, size_t n, 
 
 template <int BD, int BN, int MODE>
 static cudaError_t launch_cf(const OqCodecParams& p, const void* x, int dtype, size_t n,
-                             uint8_t* out, uint32_t* flag_idx, uint32_t* flag_cnt,
+                             uint8_t* out, FlagEntry* flag_idx, uint32_t* flag_cnt,
                              cudaStream_t st, int num_sms) {
   if (dtype == OQ_BF16)
     return launch_cf_t<BD, BN, MODE, OQ_BF16>(p, x, n, out, flag_idx, flag_cnt, st, num_sms);
@@ -411,7 +431,7 @@ bool compress_fast_ok(const OqCodecParams& p, int dtype, const void* x, const vo
 }
 
 cudaError_t launch_compress_fast(const OqCodecParams& p, const void* x, int dtype, size_t n,
-                                 uint8_t* out, uint32_t* flag_idx, uint32_t* flag_cnt,
+                                 uint8_t* out, FlagEntry* flag_idx, uint32_t* flag_cnt,
                                  cudaStream_t st, int num_sms) {
 #define OQ_CF(BD, BN)                                                                          \
   if (p.b_dir == BD && p.b_nrm == BN)                                                          \

@@ -143,35 +143,18 @@ __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const Co
   return bx | (by << 8) | (ir << 16);
 }
 
-// One key (d = 128, no QJL) by one warp, latency first.  Lane l holds
-// coordinates 4l .. 4l+3 in fp64; gamma is lane 0's sequential sum over the
-// shared row (codec.hpp:219-221); signs + WHT use the reference's butterfly
-// pairs (two in-lane stages, five shuffle stages); lane l then rounds
-// triplets l and l + 32 with joint_round reading the codec tables straight
-// from global memory (L1-resident: no per-CTA staging), and the fields are
-// OR-ed into the record words rec[0 .. 31] (codec.hpp:381-393).  row: 132
-// doubles of warp-private shared scratch.  Ends with a __syncwarp.
-__device__ __forceinline__ void encode_key_warp(const OqCodecParams& p, const void* __restrict__ x,
-                                                int dtype, size_t key, double* row, uint32_t* rec,
-                                                int lane) {
+// The reference's rotated, padded coordinates of one d = 128 key by one warp
+// (Encoder::encode, codec.hpp:222-230): u = k * inv, signs, WHT with the
+// reference's butterfly pairs (two in-lane stages, five shuffle stages), *
+// 1/sqrt(d) -> row[0 .. 129) (row[128] = 0, the pad).  Lane l holds
+// coordinates 4l .. 4l+3.  Ends with a __syncwarp.
+__device__ __forceinline__ void rotate_key_warp(const OqCodecParams& p, const double (&k)[4],
+                                                double inv, double* row, int lane) {
   double v[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    v[i] = load_as_double(x, dtype, key * 128 + 4 * lane + i);
-    row[4 * lane + i] = dmul(v[i], v[i]);
-  }
-  rec[lane] = 0u;
-  __syncwarp();
-  double g2 = 0.0;  // squares are rounded identically in parallel: only the adds chain
-  if (lane == 0)
-    for (int e = 0; e < 128; ++e) g2 = dadd(g2, row[e]);
-  g2 = __shfl_sync(kFull, g2, 0);
-  const double gamma = dsqrt(g2);
-  const double inv = ddiv(1.0, gamma > 1e-12 ? gamma : 1e-12);
   // u = k * inv, signs, fwht (rotation.hpp:20-31, 46-49)
   const uint32_t sm = p.sign_mask[lane >> 3] >> (4 * (lane & 7));
 #pragma unroll
-  for (int i = 0; i < 4; ++i) v[i] = dflip(dmul(v[i], inv), (sm >> i) & 1u);
+  for (int i = 0; i < 4; ++i) v[i] = dflip(dmul(k[i], inv), (sm >> i) & 1u);
   {
     double a = v[0], b = v[1];
     v[0] = dadd(a, b); v[1] = dsub(a, b);
@@ -196,8 +179,40 @@ __device__ __forceinline__ void encode_key_warp(const OqCodecParams& p, const vo
   for (int i = 0; i < 4; ++i) row[4 * lane + i] = dmul(v[i], p.inv_sqrt_d);
   if (lane == 0) row[128] = 0.0;  // zero pad to 3 * n_tri (codec.hpp:229-230)
   __syncwarp();
-  const CompressSmem tabs{const_cast<double*>(p.xi_bnd), const_cast<double*>(p.rho_bnd),
-                          const_cast<double*>(p.rho_c), p.dirs64, p.xi_lut, p.rho_lut};
+}
+
+// The codebook tables joint_round reads, straight from global memory.
+__device__ __forceinline__ CompressSmem global_tables(const OqCodecParams& p) {
+  return CompressSmem{const_cast<double*>(p.xi_bnd), const_cast<double*>(p.rho_bnd),
+                      const_cast<double*>(p.rho_c), p.dirs64, p.xi_lut, p.rho_lut};
+}
+
+// One key (d = 128, no QJL) by one warp, latency first.  gamma is lane 0's
+// sequential sum over the shared row (codec.hpp:219-221); rotate_key_warp;
+// lane l then rounds triplets l and l + 32 with joint_round reading the codec
+// tables straight from global memory (L1-resident: no per-CTA staging), and
+// the fields are OR-ed into the record words rec[0 .. 31] (codec.hpp:381-393).
+// row: 132 doubles of warp-private shared scratch.  Ends with a __syncwarp.
+__device__ __forceinline__ void encode_key_warp(const OqCodecParams& p, const void* __restrict__ x,
+                                                int dtype, size_t key, double* row, uint32_t* rec,
+                                                int lane) {
+  double k[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    k[i] = load_as_double(x, dtype, key * 128 + 4 * lane + i);
+    row[4 * lane + i] = dmul(k[i], k[i]);
+  }
+  rec[lane] = 0u;
+  __syncwarp();
+  double g2 = 0.0;  // squares are rounded identically in parallel: only the adds chain
+  if (lane == 0)
+    for (int e = 0; e < 128; ++e) g2 = dadd(g2, row[e]);
+  g2 = __shfl_sync(kFull, g2, 0);
+  const double gamma = dsqrt(g2);
+  const double inv = ddiv(1.0, gamma > 1e-12 ? gamma : 1e-12);
+  __syncwarp();
+  rotate_key_warp(p, k, inv, row, lane);
+  const CompressSmem tabs = global_tables(p);
   const float4* d32 = reinterpret_cast<const float4*>(p.dirs32);
   const int pb = 2 * p.b_dir, nb = p.b_nrm;
   for (int t = lane; t < 43; t += 32) {

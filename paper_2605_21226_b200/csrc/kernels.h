@@ -9,9 +9,9 @@
 namespace oqd {
 
 // K1: Encoder::encode -> OCTO v1 records.  d = 128 fp32 keys at the BASELINE
-// bit splits take the certified fp32 pass (compress_fast.cu) and re-encode
-// the keys it flags exactly; `flagged` (device u32, optional) receives how
-// many keys took the exact path.
+// bit splits take the certified fp32 pass (compress_fast.cu) and re-round the
+// triplets it could not decide exactly; `flagged` (device u32, optional)
+// receives how many keys had such triplets.
 cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, size_t n,
                             uint8_t* out, cudaStream_t st, int num_sms,
                             uint32_t* flagged = nullptr);
@@ -19,9 +19,22 @@ bool compress_fast_ok(const OqCodecParams& p, int dtype, const void* x, const vo
 cudaError_t launch_compress_x2(const OqCodecParams& p, const void* x, int dtype, size_t n,
                                uint8_t* out, cudaStream_t st, int num_sms,
                                const uint32_t* list = nullptr, const uint32_t* list_n = nullptr);
+// A key the certified fp32 pass could not fully decide: the triplets whose
+// decisions missed their margin (mask bit t; all 43 for a key-level miss)
+// and the exact fp64 1 / max(gamma, 1e-12) (codec.hpp:222).
+struct FlagEntry {
+  uint32_t key, mlo, mhi, pad;
+  double inv, pad2;
+};
 cudaError_t launch_compress_fast(const OqCodecParams& p, const void* x, int dtype, size_t n,
-                                 uint8_t* out, uint32_t* flag_idx, uint32_t* flag_cnt,
+                                 uint8_t* out, FlagEntry* flags, uint32_t* flag_cnt,
                                  cudaStream_t st, int num_sms);
+// Exact re-encode of the flagged triplets only (one warp per flagged key:
+// fp64 rotation from the stored inv, joint_round per flagged triplet, fields
+// patched into the record in place).
+cudaError_t launch_compress_fixup(const OqCodecParams& p, const void* x, int dtype, uint8_t* out,
+                                  const FlagEntry* flags, const uint32_t* flag_cnt,
+                                  cudaStream_t st, int num_sms);
 // K2: Encoder::decode of OCTO v1 records -> fp32 [n, dim].
 cudaError_t launch_decode(const OqCodecParams& p, const uint8_t* recs, size_t n, float* out,
                           cudaStream_t st, int num_sms);
