@@ -229,11 +229,11 @@ __global__ void __launch_bounds__(256) decode_kernel(OqCodecParams p,
 // registers; the whole inverse WHT (7 butterfly stages) runs in registers
 // with no shuffles, signs and gamma/sqrt(d) are folded into one multiply per
 // coordinate, and each warp transposes its 32 decoded keys through shared
-// memory (two 64-coordinate halves) so that global stores are 256-byte
+// memory (four 32-coordinate quarters) so that global stores are 128-byte
 // segments.  Shared traffic per key: record staging, 43 direction + 43 norm
 // lookups and the output transpose.
 constexpr int kD128Threads = 128;            // 4 warps, 128 keys per block
-constexpr int kD128HalfStride = 68;          // floats per staged half row (64 + 4)
+constexpr int kD128HalfStride = 36;          // floats per staged quarter row (32 + 4)
 
 template <int BD, int BN>
 struct D128 {
@@ -387,23 +387,24 @@ __global__ void __launch_bounds__(kD128Threads, 3) decode128_kernel(OqCodecParam
       const bool neg = (p.sign_mask[i >> 5] >> (i & 31)) & 1u;  // uniform
       y[i] *= neg ? -gs : gs;
     }
-    // ---- per-warp transpose through shared memory, two halves ----------------
+    // ---- per-warp transpose through shared memory, four quarters -----------
+    // (a 32-float staging row per lane keeps the block at 3 CTAs per SM)
     const int kw0 = warp * 32;  // this warp's first key in the block
     const int nkw = min(32, nv - kw0);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < 4; ++h) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
+      for (int i = 0; i < 8; ++i)
         *reinterpret_cast<float4*>(hs + lane * kD128HalfStride + 4 * i) =
-            make_float4(y[64 * h + 4 * i], y[64 * h + 4 * i + 1], y[64 * h + 4 * i + 2],
-                        y[64 * h + 4 * i + 3]);
+            make_float4(y[32 * h + 4 * i], y[32 * h + 4 * i + 1], y[32 * h + 4 * i + 2],
+                        y[32 * h + 4 * i + 3]);
       __syncwarp();
-      // 32 keys x 16 float4 of this half: lane -> (key = it*2 + lane/16, f4 = lane%16)
+      // 32 keys x 8 float4 of this quarter: lane -> (key = it*4 + lane/8, f4 = lane%8)
       if (nkw > 0) {
-        float* ob = out + (v0 + kw0) * 128 + 64 * h;
+        float* ob = out + (v0 + kw0) * 128 + 32 * h;
 #pragma unroll 4
-        for (int it = 0; it < 16; ++it) {
-          const int k = 2 * it + (lane >> 4), f = lane & 15;
+        for (int it = 0; it < 8; ++it) {
+          const int k = 4 * it + (lane >> 3), f = lane & 7;
           if (k < nkw) {
             const float4 v = *reinterpret_cast<const float4*>(hs + k * kD128HalfStride + 4 * f);
             __stcs(reinterpret_cast<float4*>(ob + (size_t)k * 128) + f, v);
