@@ -173,6 +173,39 @@ def build_cache(oq, torch, dev, bits, qjl, B, Hkv, T, seed, keep_host=0):
     return cache, host
 
 
+def other_configs(oq, torch, dev, peak, main_cfg, steps=20):
+    """K3 at the BASELINE configs other than the headline one (single GPU,
+    same method: device-resident cache, library CUDA events around K3)."""
+    res = {}
+    for name, (bits, qjl, B, Hq, Hkv, T, desc) in WORKLOADS.items():
+        if name == main_cfg:
+            continue
+        cache, _ = build_cache(oq, torch, dev, bits, qjl, B, Hkv, T, seed=7)
+        q = torch.randn((B, Hq, 128), device=dev, generator=torch.Generator(device=dev).manual_seed(5))
+        out = torch.empty((B, Hq, 128), dtype=torch.float32, device=dev)
+        for _ in range(3):
+            oq.attention_decode(q, cache, n_splits=0, out=out)
+        torch.cuda.synchronize()
+        oq.timing(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            oq.attention_decode(q, cache, n_splits=0, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        k_ms, k_n = oq.timing_collect("attention")
+        oq.timing(False)
+        kern = k_ms / max(1, k_n)
+        nbytes = B * Hkv * T * (rec_bytes(bits, qjl) + rec_bytes(bits, False))
+        res[name] = {"workload": desc, "algorithmic_bytes": nbytes,
+                     "step_us": e0.elapsed_time(e1) / steps * 1e3, "kernel_us": kern * 1e3,
+                     "kernel_gbs": nbytes / (kern * 1e-3) / 1e9,
+                     "frac": nbytes / (kern * 1e-3) / 1e9 / peak}
+        del cache
+        torch.cuda.empty_cache()
+    return res
+
+
 def cpu_reference_sample(ref_lib, bits, qjl, seed, k_recs, v_recs, q, threads):
     """One bounded sample of the workload on the reference CPU implementation:
     Encoder::decode of the V records + attention_decode for every query head
@@ -268,6 +301,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-compress", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the K3 timings at the non-headline BASELINE configs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -421,6 +456,11 @@ def main():
     if not args.no_compress:
         comp = bench_compress(oq, torch, dev, bits, world, barrier, dist, peak)
 
+    # ---- K3 at the other BASELINE configs (C4 QJL, C5 2-bit) ---------------------
+    others = None
+    if world == 1 and not args.no_other_configs:
+        others = other_configs(oq, torch, dev, peak, args.config)
+
     # ---- CPU baseline: the reference implementation on this host ----------------
     cpu = None
     if keep:
@@ -469,6 +509,7 @@ def main():
             "gpu_launches": (1 if world == 1 else 4) * args.steps,
             "compress": comp,
             "decode_step": step_info,
+            "other_configs": others,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

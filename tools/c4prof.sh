@@ -1,7 +1,7 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 timeout 600 python bench.py --no-cpu-baseline --steps 50 > gpurun_out/b_c3.log 2>&1
-for c in c4 c5; do timeout 600 python bench.py --no-cpu-baseline --no-compress --steps 50 --config $c > gpurun_out/b_$c.log 2>&1; done
-timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:attn_partials -s 4 -c 1 -o gpurun_out/prof_attn_c4 -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-compress --config c4 > gpurun_out/ncu_c4.log 2>&1
+for c in c4 c5; do timeout 600 python bench.py --no-cpu-baseline --no-compress --no-other-configs --steps 50 --config $c > gpurun_out/b_$c.log 2>&1; done
+timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:attn_partials -s 4 -c 1 -o gpurun_out/prof_attn_c4 -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-compress --no-other-configs --config c4 > gpurun_out/ncu_c4.log 2>&1
 python - <<'PY'
 import json
 for f in ["gpurun_out/b_c3.log", "gpurun_out/b_c4.log", "gpurun_out/b_c5.log"]:

@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 K=${1:-"attention or codec"}
 timeout 900 python -m pytest tests -m gpu -q -x -k "$K" > gpurun_out/q_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/q_pytest.log
 timeout 600 python bench.py --no-cpu-baseline --steps 100 > gpurun_out/q_bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/q_bench.log
-timeout 600 python bench.py --no-cpu-baseline --no-compress --steps 100 --config c4 > gpurun_out/q_bench_c4.log 2>&1
+timeout 600 python bench.py --no-cpu-baseline --no-compress --no-other-configs --steps 100 --config c4 > gpurun_out/q_bench_c4.log 2>&1
 tail -3 gpurun_out/q_pytest.log
 python - <<'PY'
 import json

@@ -47,6 +47,8 @@ def main():
             f"{d['decode_step']['append_us']:.1f} µs, step {d['decode_step']['append_plus_attention_us']:.1f} µs"
             f" eager / {d['decode_step'].get('graph_append_plus_attention_us', float('nan')):.1f} µs "
             f"CUDA graph\n" if d.get("decode_step") else "\n"),
+           "".join(f"- {k.upper()} K3 ({v['workload']}): {v['kernel_us']:.1f} µs -> {v['kernel_gbs']:.0f} GB/s = "
+                   f"{100 * v['frac']:.1f} % of peak\n" for k, v in (d.get("other_configs") or {}).items()),
            "| bits | K1 compress µs | G keys/s | GB/s (% HBM) | flagged keys | K2 decode µs | GB/s (% HBM) |",
            "|---|---|---|---|---|---|---|"]
     for b, v in c["sweep_bits"].items():
