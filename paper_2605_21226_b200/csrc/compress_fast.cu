@@ -230,7 +230,23 @@ __global__ void __launch_bounds__(kCFThreads, 1)
     scr[0] = __float_as_uint(gf);
     uint64_t dacc = 0, nacc = 0;
     int dn = 0, nn = (8 * S::DIRB) & 31, dw = 1, nw = (32 + 8 * S::DIRB) >> 5;
-    auto put = [&](int wi, uint32_t v) { scr[32 * wi] |= v; };
+    // completed words are stored directly (the scratch row starts zeroed);
+    // only the word the direction and norm streams share is OR-ed
+    constexpr int SHARED_W = ((4 + S::DIRB) & 3) ? (4 + S::DIRB) >> 2 : -1;
+    auto put = [&](int wi, uint32_t v) {
+      if (wi == SHARED_W) scr[32 * wi] |= v;
+      else scr[32 * wi] = v;
+    };
+    // append `bits` (<= 32) to a stream accumulator holding n < 32 bits
+    auto append = [&](uint64_t& acc, int& n, int& w, uint64_t v, int bits) {
+      acc |= v << n;
+      n += bits;
+      if (n >= 32) {
+        put(w++, (uint32_t)acc);
+        acc >>= 32;
+        n -= 32;
+      }
+    };
 #pragma unroll 1
     for (int q = 0; q < 11; ++q) {
       float e[12];
@@ -244,6 +260,10 @@ __global__ void __launch_bounds__(kCFThreads, 1)
         e[8] = v2.x; e[9] = v2.y; e[10] = v2.z; e[11] = v2.w;
       }
       uint32_t gmask = 0;  // undecided triplets of this group of 4
+      // (4,2): a group's four 8-bit direction pairs are exactly record word
+      // q + 1 and its four 2-bit norms record byte 47 + q (stored directly)
+      uint32_t gdir = 0, gnrm = 0;
+      uint64_t gdir64 = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int t = 4 * q + j;
@@ -308,25 +328,38 @@ __global__ void __launch_bounds__(kCFThreads, 1)
         gmask |= (okt ? 0u : 1u) << j;
         // ---- append the fields (masked to their widths: an undecided
         // triplet's fields are patched in place by the exact fixup) ----------
-        dacc |= (uint64_t)((ix & (K - 1)) | ((iy & (K - 1)) << BD)) << dn;
-        dn += 2 * BD;
-        if (dn >= 32) {
-          put(dw++, (uint32_t)dacc);
-          dacc >>= 32;
-          dn -= 32;
+        const uint32_t fpair = (ix & (K - 1)) | ((iy & (K - 1)) << BD);
+        if constexpr (BD == 4 && BN == 2) {
+          gdir |= fpair << (8 * j);
+          gnrm |= ir << (2 * j);
+        } else {  // group bits at compile-time offsets, one stream append per group
+          gdir64 |= (uint64_t)fpair << (2 * BD * j);
+          gnrm |= ir << (BN * j);
         }
-        nacc |= (uint64_t)ir << nn;
-        nn += BN;
-        if (nn >= 32) {
-          put(nw++, (uint32_t)nacc);
-          nacc >>= 32;
-          nn -= 32;
+      }
+      if constexpr (!(BD == 4 && BN == 2)) {
+        const int ng = q < 10 ? 4 : S::NT - 40;  // triplets in this group
+        if (2 * BD * ng <= 32) {
+          append(dacc, dn, dw, gdir64, 2 * BD * ng);
+        } else {
+          append(dacc, dn, dw, gdir64 & 0xffffffffull, 32);
+          append(dacc, dn, dw, gdir64 >> 32, 2 * BD * ng - 32);
         }
+        append(nacc, nn, nw, gnrm, BN * ng);
+      } else {
+        static_assert(S::DIRB == 43, "record layout of (4,2)");
+        // word 11 (q = 10) holds dir bytes 44..46 and norm byte 47 (q = 0's)
+        if (q < 10) scr[32 * (q + 1)] = gdir;
+        else scr[32 * (q + 1)] |= gdir;
+        const int nb = 4 + S::DIRB + q;  // record byte of this group's norms
+        reinterpret_cast<uint8_t*>(scr + 32 * (nb >> 2))[nb & 3] = (uint8_t)gnrm;
       }
       fmask |= (uint64_t)gmask << (4 * q);
     }
-    if (dn > 0) put(dw, (uint32_t)dacc);
-    if (nn > 0) put(nw, (uint32_t)nacc);
+    if constexpr (!(BD == 4 && BN == 2)) {
+      if (dn > 0) put(dw, (uint32_t)dacc);
+      if (nn > 0) put(nw, (uint32_t)nacc);
+    }
     __syncwarp();
     if (blk + wstride < nblk) {  // the staging row is consumed: fetch the next block
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
