@@ -314,12 +314,19 @@ def main():
     import paper_2605_21226_b200 as oq
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    # OQ_BENCH_SHARDED=1 runs the sequence-sharded step (partials + NCCL
+    # all-gather + merge) even on one rank: the N>1 code path, testable on 1 GPU
+    sharded = world > 1 or os.environ.get("OQ_BENCH_SHARDED") == "1"
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if sharded:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+        dist.init_process_group("nccl", device_id=dev, world_size=world, rank=rank)
 
     bits, qjl, B, Hq, Hkv, T, desc = WORKLOADS[args.config]
     keep = Hkv if (rank == 0 and world == 1 and not args.no_cpu_baseline) else 0
@@ -333,7 +340,7 @@ def main():
     out = torch.empty((B, Hq, 128), dtype=torch.float32, device=dev)
 
     def step(qd):
-        if world == 1:
+        if not sharded:
             return oq.attention_decode(qd, cache, n_splits=splits, out=out)
         part = oq.attention_partials(qd, cache, 0, T, n_splits=splits)
         dist.all_gather_into_tensor(gathered, part)
@@ -506,13 +513,13 @@ def main():
             "clocks": clk.summary(),
             # world 1: one fused K3 launch per step; sharded: K5 + K3 + local
             # merge + final merge around the NCCL all-gather
-            "gpu_launches": (1 if world == 1 else 4) * args.steps,
+            "gpu_launches": (4 if sharded else 1) * args.steps,
             "compress": comp,
             "decode_step": step_info,
             "other_configs": others,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.barrier()
         dist.destroy_process_group()
     return 0

@@ -61,7 +61,7 @@ def main():
     out.append("## K3, `ncu --set full`\n")
     out.append(run("full", os.path.join(g, "prof_attn.ncu-rep"), "--units", "131072", "--unit-name",
                    "tile"))
-    out.append("## K1 (certified-fp32 pass + exact re-encode of the flagged keys) and K2, "
+    out.append("## K1 (certified-fp32 pass + exact re-rounding of the undecided triplets) and K2, "
                "`ncu --set full` (2^20 keys, b=3)\n")
     out.append(run("full", os.path.join(g, "prof_codec.ncu-rep")))
     open(os.path.join(ROOT, "profiles", f"{name}_summary.md"), "w").write("\n".join(out))
