@@ -258,8 +258,9 @@ struct AttnKParams {
   // fragments itself from q and finalises each stream's rows once its last
   // partial lands (per-stream arrival counters, left at zero)
   int fuse, qjl;
+  int out_partial;       // fused: write merged (m, l, 0, 0, acc) rows of kPartW floats
   const float* q;        // [B, Hq, 128]
-  float* out;            // [B * Hq, 128]
+  float* out;            // [B * Hq, 128] (or [B * Hq, kPartW] with out_partial)
   uint32_t* counters;    // [n_sh], zero on entry and exit
   uint32_t smask[4], qmask[4], vmask[4];
   float inv_sqrt_d;
@@ -679,9 +680,11 @@ __device__ __forceinline__ void seg_qprep(uint32_t (&qf)[QF], const AttnKParams&
 
 // Fused K4 for one row: merge its n partials in order (SoftmaxState::merge,
 // attention.hpp:36-44), acc / l, inverse V rotation; one warp.
+// partial: write the merged state (M, L, 0, 0, acc[128]) (the format of
+// combine_kernel's finalize = 0, for a later cross-rank merge) instead.
 __device__ __forceinline__ void combine_row(const float* base, int n, float* out,
                                             const uint32_t (&vmask)[4], float inv_sqrt_d,
-                                            int lane) {
+                                            int lane, bool partial = false) {
   const float NEG_INF = -__int_as_float(0x7f800000);
   float M = NEG_INF;
   for (int i = lane; i < n; i += 32) {
@@ -699,6 +702,11 @@ __device__ __forceinline__ void combine_row(const float* base, int n, float* out
       const float4 a4 = *reinterpret_cast<const float4*>(base + (size_t)i * kPartW + 4 + 4 * lane);
       y[0] += a4.x * f; y[1] += a4.y * f; y[2] += a4.z * f; y[3] += a4.w * f;
     }
+  }
+  if (partial) {
+    if (lane == 0) *reinterpret_cast<float4*>(out) = make_float4(M, L, 0.f, 0.f);
+    *reinterpret_cast<float4*>(out + 4 + 4 * lane) = make_float4(y[0], y[1], y[2], y[3]);
+    return;
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;
 #pragma unroll
@@ -780,8 +788,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
         for (int w = warp; w < 8; w += kAttnWarps) {
           if (8 * it.hc + w >= P.G) continue;
           const size_t row = (size_t)it.b * P.Hq + (size_t)it.kvh * P.G + 8 * it.hc + w;
-          combine_row(P.partials + row * P.n_parts * kPartW, nparts, P.out + row * 128, P.vmask,
-                      P.inv_sqrt_d, lane);
+          combine_row(P.partials + row * P.n_parts * kPartW, nparts,
+                      P.out + row * (P.out_partial ? kPartW : 128), P.vmask, P.inv_sqrt_d, lane,
+                      P.out_partial);
         }
       }
     }
@@ -1323,6 +1332,7 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
     P.tps = tz > P.tb0 ? tz - P.tb0 : 0;
   }
   P.fuse = a.out != nullptr && a.counters != nullptr;
+  P.out_partial = a.out_partial;
   P.qjl = pk.qjl;
   P.q = a.q;
   P.out = a.out;

@@ -564,7 +564,8 @@ static oq_status attn_check(const oq_codec* ck, const oq_codec* cv, const oq_att
 static oq_status run_partials(const oq_codec* ck, const oq_codec* cv, const oq_attn_shape* sh,
                               const float* q, const void* kc, const void* vc, uint64_t t0,
                               uint64_t t1, int n_splits, void* ws, cudaStream_t st,
-                              float** parts_out, int* n_parts_out, float* fused_out = nullptr) {
+                              float** parts_out, int* n_parts_out, float* fused_out = nullptr,
+                              bool fused_partial = false) {
   const size_t rows = (size_t)sh->B * sh->Hq;
   const int np_max = parts_per_row(ck, sh, 0, sh->T, n_splits) + 1;
   const int np = parts_per_row(ck, sh, t0, t1, n_splits);
@@ -586,6 +587,15 @@ static oq_status run_partials(const oq_codec* ck, const oq_codec* cv, const oq_a
   a.n_parts = np;
   *n_parts_out = np;
   a.qfrag = w8 + kCounterBytes + ((part + 255) & ~size_t(255));
+  if (t1 <= t0) {  // no tokens in range: every row's partial is empty (l = 0)
+    const size_t w = 4 + ck->cfg.dim;
+    float* dst = fused_out && fused_partial ? fused_out : a.partials;
+    const size_t nrow = fused_out && fused_partial ? rows : rows * (size_t)np;
+    const cudaError_t z = cudaMemsetAsync(dst, 0, nrow * w * sizeof(float), st);
+    if (z != cudaSuccess) return cuda_fail(z, "cudaMemsetAsync");
+    *parts_out = fused_out && fused_partial ? nullptr : a.partials;
+    return OQ_OK;
+  }
   // one launch when the per-stream counters fit: q prep and the final merge
   // run inside the attention kernel
   const size_t n_sh = (size_t)sh->B * sh->Hkv * ((sh->Hq / sh->Hkv + 7) / 8);
@@ -593,6 +603,7 @@ static oq_status run_partials(const oq_codec* ck, const oq_codec* cv, const oq_a
   cudaError_t e = cudaSuccess;
   if (fuse) {
     a.out = fused_out;
+    a.out_partial = fused_partial ? 1 : 0;
     a.counters = reinterpret_cast<uint32_t*>(w8);
     for (int i = 0; i < 4; ++i) a.vmask[i] = cv->p.sign_mask[i];
   } else {
@@ -682,8 +693,11 @@ oq_status oq_attention_partials(const oq_codec* ck, const oq_codec* cv, const oq
   if (t0 > t1 || t1 > sh->T) return fail(OQ_ERR_INVALID_ARGUMENT, "bad token range");
   float* parts = nullptr;
   int np = 0;
-  s = run_partials(ck, cv, sh, q, kc, vc, t0, t1, n_splits, ws, as_stream(stream), &parts, &np);
-  if (s) return s;
+  // one launch when possible: the attention kernel merges its splits into
+  // the (m, l, acc) partial itself
+  s = run_partials(ck, cv, sh, q, kc, vc, t0, t1, n_splits, ws, as_stream(stream), &parts, &np,
+                   partial, true);
+  if (s || !parts) return s;
   const int rows = sh->B * sh->Hq;
   const size_t w = 4 + ck->cfg.dim;
   cudaError_t e = oqd::launch_attention_combine(cv->p, parts, rows, np, np * w, w, 0,
@@ -735,12 +749,18 @@ oq_status oq_attention_decode_sharded(const oq_codec* ck, const oq_codec* cv,
   float* gather = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + ((base + 255) & ~size_t(255)));
   float* parts = nullptr;
   int np = 0;
-  s = run_partials(ck, cv, sh, q, kc, vc, t0, t1, n_splits, ws, st, &parts, &np);
+  // this rank's merged partial lands straight in its slot of the gather
+  // buffer: from the attention kernel itself when it runs fused, else by a
+  // combine pass over its splits
+  s = run_partials(ck, cv, sh, q, kc, vc, t0, t1, n_splits, ws, st, &parts, &np,
+                   gather + (size_t)rank * per, true);
   if (s) return s;
-  // merge this rank's splits straight into its slot of the gather buffer
-  cudaError_t e = oqd::launch_attention_combine(cv->p, parts, rows, np, np * w, w, 0,
-                                                gather + (size_t)rank * per, st);
-  if (e != cudaSuccess) return cuda_fail(e, "combine kernel");
+  cudaError_t e = cudaSuccess;
+  if (parts) {
+    e = oqd::launch_attention_combine(cv->p, parts, rows, np, np * w, w, 0,
+                                      gather + (size_t)rank * per, st);
+    if (e != cudaSuccess) return cuda_fail(e, "combine kernel");
+  }
   // the only collective: in-place all-gather of the per-rank partials
   if ((r = api.all_gather(gather + (size_t)rank * per, gather, per, /*ncclFloat32*/ 7, comm, st)) != 0)
     return nccl_fail(r, "ncclAllGather");

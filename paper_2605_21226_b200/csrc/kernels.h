@@ -60,6 +60,7 @@ struct AttnArgs {
   // fused single-launch mode (attention_decode on one GPU): when both are set
   // the attention kernel prepares q itself and writes the final rows to out
   uint32_t* counters = nullptr;  // [B*Hkv*ceil(G/8)] zero on entry, left zero
+  int out_partial = 0;  // fused: out rows are merged (m, l, 0, 0, acc[D]) partials
   uint32_t vmask[4] = {0, 0, 0, 0};  // V rotation signs (for the fused combine)
 };
 

@@ -65,3 +65,21 @@ def test_rank_ordered_merge_matches_n_splits(cuda, P):
     # P fragments are rounded to fp16 against different running maxima when
     # the split points differ, hence the same 1e-3 bound between them
     assert err < 1e-3, err
+
+
+def test_empty_rank_range_is_an_empty_partial(cuda):
+    """A rank whose token range is empty contributes an empty (l = 0) partial
+    (attention.hpp:40-41 skips it in the merge)."""
+    import torch
+    B, Hkv, T = 1, 2, 65
+    cache, q = _cache(cuda, B, Hkv, T)
+    rows = B * 7 * Hkv
+    ranges = [(0, 40), (40, 65), (65, 65)]
+    parts = [oq.attention_partials(q, cache, t0, t1) for t0, t1 in ranges]
+    assert float(parts[2][:, 1].abs().max()) == 0.0  # l = 0 on every row
+    gathered = torch.stack(parts)
+    merged = oq.attention_combine(cache.enc_v, gathered, rows, len(ranges), gathered.shape[2],
+                                  rows * gathered.shape[2])
+    want = oq.attention_decode(q, cache).reshape(rows, 128)
+    err = ((merged - want).norm(dim=-1) / want.norm(dim=-1)).max().item()
+    assert err < 1e-3, err
