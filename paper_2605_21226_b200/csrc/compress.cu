@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps) compress_small_kernel(
 // and norm fields into the record in place — the pass masks every field to
 // its width, so the other fields are already final.  Records of different
 // keys may share a 32-bit word, hence atomic clear + set on disjoint bits.
-constexpr int kFixWarps = 16, kFixKeys = 4, kFixQ = 896;
+constexpr int kFixWarps = 8, kFixKeys = 16, kFixQ = 896;
 
 struct FixTriplet {
   double t0, t1, t2;
@@ -383,14 +383,19 @@ __device__ __forceinline__ void fix_triplet(const OqCodecParams& p, const Compre
   patch_field(words, base + 32 + 8 * (size_t)p.dir_bytes + (size_t)nb * q.t, nb, ir);
 }
 
-__global__ void __launch_bounds__(32 * kFixWarps, 1) compress_fixup_kernel(
+__global__ void __launch_bounds__(32 * kFixWarps, 2) compress_fixup_kernel(
     OqCodecParams p, const void* __restrict__ x, int dtype, uint8_t* __restrict__ out,
     const FlagEntry* __restrict__ flags, const uint32_t* __restrict__ flag_cnt) {
+  extern __shared__ __align__(128) uint8_t fix_stage[];  // [kFixWarps][kFixKeys][row bytes]
   __shared__ double row_s[kFixWarps][132];
   __shared__ FixTriplet queue[kFixQ];
   __shared__ uint32_t qn;
+  __shared__ __align__(8) uint64_t bars[kFixWarps];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t n = *flag_cnt;
+  const uint32_t rbytes = 128u * (dtype == OQ_F32 ? 4u : 2u);
+  uint8_t* stage = fix_stage + (size_t)wib * kFixKeys * rbytes;
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&bars[wib]);
   {
     // warm this SM's L1 with the codebook tables: joint_round's lookups form
     // a dependent chain that would otherwise pay an L2 round trip per step
@@ -410,40 +415,67 @@ __global__ void __launch_bounds__(32 * kFixWarps, 1) compress_fixup_kernel(
       pf(p.rho_c);
       qn = 0;
     }
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
   }
   __syncthreads();
   const CompressSmem tabs = global_tables(p);
   const float4* d32 = reinterpret_cast<const float4*>(p.dirs32);
   uint32_t* words = reinterpret_cast<uint32_t*>(out);
-  constexpr size_t PER_CTA = (size_t)kFixWarps * kFixKeys;
-  for (size_t e0 = blockIdx.x * PER_CTA; e0 < n; e0 += (size_t)gridDim.x * PER_CTA) {
-    // ---- rotations: this warp's keys, all rows requested up front ----------
-    const size_t w0 = e0 + (size_t)wib * kFixKeys;
-    FlagEntry f[kFixKeys];
-    double k[kFixKeys][4];
+  // keys per warp and round: as many as the list allows up to kFixKeys, so
+  // short lists still spread over every warp
+  const size_t nwarps = (size_t)gridDim.x * kFixWarps;
+  const int kpw = (int)min((size_t)kFixKeys, max((size_t)1, (n + nwarps - 1) / nwarps));
+  const size_t per_cta = (size_t)kFixWarps * kpw;
+  uint32_t phase = 0;
+  for (size_t e0 = blockIdx.x * per_cta; e0 < n; e0 += (size_t)gridDim.x * per_cta) {
+    // ---- this warp's keys: flag entries, then their rows by 1-D TMA ------
+    const size_t w0 = e0 + (size_t)wib * kpw;
+    const int nk = (int)min((size_t)kpw, w0 < n ? n - w0 : (size_t)0);
+    FlagEntry f{};
+    if (lane < nk) f = flags[w0 + lane];
+    if (nk > 0) {
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(nk * rbytes)
+                     : "memory");
+      __syncwarp();
+      if (lane < nk)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"((uint32_t)__cvta_generic_to_shared(stage + lane * rbytes)),
+            "l"(static_cast<const uint8_t*>(x) + (size_t)f.key * rbytes), "r"(rbytes), "r"(bar)
+            : "memory");
+      asm volatile(
+          "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+          " @!p bra W_%=;\n}" ::"r"(bar),
+          "r"(phase)
+          : "memory");
+      phase ^= 1u;
+    }
+    // ---- rotations; flagged triplets -> the queue ---------------------------
+#pragma unroll 1
+    for (int j = 0; j < nk; ++j) {
+      const uint32_t key = __shfl_sync(kFull, f.key, j), mlo = __shfl_sync(kFull, f.mlo, j),
+                     mhi = __shfl_sync(kFull, f.mhi, j);
+      const double inv = __shfl_sync(kFull, f.inv, j);
+      double k[4];
 #pragma unroll
-    for (int j = 0; j < kFixKeys; ++j)
-      if (w0 + j < n) f[j] = flags[w0 + j];
-#pragma unroll
-    for (int j = 0; j < kFixKeys; ++j)
-      if (w0 + j < n)
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          k[j][i] = load_as_double(x, dtype, (size_t)f[j].key * 128 + 4 * lane + i);
-#pragma unroll
-    for (int j = 0; j < kFixKeys; ++j) {
-      if (w0 + j >= n) break;
-      rotate_key_warp(p, k[j], f[j].inv, row_s[wib], lane);
+      for (int i = 0; i < 4; ++i) k[i] = load_as_double(stage + j * rbytes, dtype, 4 * lane + i);
+      rotate_key_warp(p, k, inv, row_s[wib], lane);
       const double* row = row_s[wib];
       for (int t = lane; t < 43; t += 32) {
-        if (!(((t < 32 ? f[j].mlo >> t : f[j].mhi >> (t - 32))) & 1u)) continue;
-        const FixTriplet q{row[3 * t], row[3 * t + 1], row[3 * t + 2], f[j].key, (uint32_t)t};
+        if (!(((t < 32 ? mlo >> t : mhi >> (t - 32))) & 1u)) continue;
+        const FixTriplet q{row[3 * t], row[3 * t + 1], row[3 * t + 2], key, (uint32_t)t};
         const uint32_t slot = atomicAdd(&qn, 1u);
         if (slot < kFixQ) queue[slot] = q;
         else fix_triplet(p, tabs, d32, words, q);  // queue full: decide it here
       }
       __syncwarp();
     }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging reused by TMA
     __syncthreads();
     // ---- decisions: one queued triplet per thread -------------------------
     const uint32_t m = min(qn, (uint32_t)kFixQ);
@@ -458,7 +490,10 @@ cudaError_t launch_compress_fixup(const OqCodecParams& p, const void* x, int dty
                                   const FlagEntry* flags, const uint32_t* flag_cnt,
                                   cudaStream_t st, int num_sms) {
   // the count lives on the device: a fixed persistent grid strides over it
-  compress_fixup_kernel<<<num_sms, 32 * kFixWarps, 0, st>>>(p, x, dtype, out, flags, flag_cnt);
+  const int sm = kFixWarps * kFixKeys * 128 * 4;
+  cudaError_t e = set_smem_once(compress_fixup_kernel, sm);
+  if (e != cudaSuccess) return e;
+  compress_fixup_kernel<<<2 * num_sms, 32 * kFixWarps, sm, st>>>(p, x, dtype, out, flags, flag_cnt);
   return cudaGetLastError();
 }
 
