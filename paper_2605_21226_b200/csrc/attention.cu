@@ -395,11 +395,16 @@ __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL
     if (QJL) {
       // residual sketch: sum_i (+-1)_i q_sketch_i on the tensor cores
       const uint32_t w0 = ~(st ? R.sg.z : R.sg.x), w1 = ~(st ? R.sg.w : R.sg.y);
-      float e[4] = {0.f, 0.f, 0.f, 0.f};
+      // two independent accumulation chains (the 8 sign MMAs would otherwise
+      // form one serial dependency chain per sub-tile)
+      float e[4] = {0.f, 0.f, 0.f, 0.f}, e2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int kb = 0; kb < 8; ++kb)
-        mma16816(e, sign_pair(w0, 2 * kb), sign_pair(w1, 2 * kb), sign_pair(w0, 2 * kb + 1),
-                 sign_pair(w1, 2 * kb + 1), qf[18 + 2 * kb], qf[18 + 2 * kb + 1]);
+        mma16816(kb & 1 ? e2 : e, sign_pair(w0, 2 * kb), sign_pair(w1, 2 * kb),
+                 sign_pair(w0, 2 * kb + 1), sign_pair(w1, 2 * kb + 1), qf[18 + 2 * kb],
+                 qf[18 + 2 * kb + 1]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) e[i] += e2[i];
       const uint32_t grw = st ? R.gr.y : R.gr.x;
       const float gr0 = __half2float(__ushort_as_half((unsigned short)(grw & 0xffff)));
       const float gr1 = __half2float(__ushort_as_half((unsigned short)(grw >> 16)));
