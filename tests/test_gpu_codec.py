@@ -199,3 +199,45 @@ def test_small_batch_kernel_bit_exact(orc, cuda, cfg, dtype):
             eo.encode_f32(xs.astype(np.float32))
         bad = np.nonzero((got != want).any(1))[0]
         assert bad.size == 0, f"n={n}: {bad.size} mismatching records, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("b", [2, 3, 4])
+@pytest.mark.parametrize("rounding", ["local3x3", "scalar"])
+def test_fast_path_special_keys_bit_exact(orc, cuda, b, rounding):
+    """Batches large enough for the certified fp32 pass (> 8192 keys) with the
+    keys it cannot certify at all mixed in: zero keys, norms outside
+    [2^-60, 2^60] (every triplet goes to the exact fixup), basis vectors
+    (exact ties in the 3x3 window), tiny triplets next to large ones, and
+    inf / NaN coordinates — all bit-exact against the CPU reference."""
+    import torch
+    n = 20000
+    bd, bn = oq.default_bit_split(b)
+    x = orc.gaussian_f32(orc.L.orc_stream_child(77 + b, 0), n * 128).reshape(n, 128)
+    rng = np.random.default_rng(b)
+    idx = rng.choice(n, 64, replace=False)
+    for j, i in enumerate(idx):
+        kind = j % 8
+        if kind == 0:
+            x[i] = 0.0
+        elif kind == 1:
+            x[i] *= 1e-25
+        elif kind == 2:
+            x[i] *= 1e25
+        elif kind == 3:
+            x[i] = 0.0
+            x[i, j % 128] = 3.0
+        elif kind == 4:
+            x[i, : 3 * (j % 40)] *= 1e-6  # tiny leading triplets
+        elif kind == 5:
+            x[i, j % 128] = np.inf
+        elif kind == 6:
+            x[i, j % 128] = np.nan
+        else:
+            x[i, 0::3] = x[i, 1::3]  # many equal |t0| = |t1| folds
+    enc = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rounding=rounding))
+    fl = torch.zeros(1, dtype=torch.int32, device=cuda)
+    got = enc.compress(torch.from_numpy(x).to(cuda), flagged=fl).cpu().numpy()
+    want = orc.encoder(b_dir=bd, b_nrm=bn, rounding=rounding).encode_f32(x, threads=os.cpu_count() or 8)
+    bad = np.nonzero((got != want).any(1))[0]
+    assert bad.size == 0, f"{bad.size} records differ, first {bad[:5]} ({int(fl.item())} flagged)"
+    assert int(fl.item()) >= 40  # the special keys all went through the fixup
