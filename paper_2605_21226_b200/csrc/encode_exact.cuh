@@ -129,15 +129,40 @@ __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const Co
       return wa | (wb << 8) | (ir << 16);
     }
   }
-  for (uint32_t a = ax0; a <= ax1; ++a)
-    for (uint32_t b = ay0; b <= ay1; ++b) {
-      const double sc = dot3_exact(t0, t1, t2, s.dirs + 3 * (a * K + b));
-      if (sc > best) {  // strict: ties keep the first row-major pair
-        best = sc;
-        bx = a;
-        by = b;
+  if (p.rounding == 2) {
+    // the clamped 3x3 window as a fixed 3x3 with invalid cells skipped: the
+    // nine exact dot products are independent (issued together), the
+    // strict-'>' scan over them stays in row-major order
+    double sc[3][3];
+#pragma unroll
+    for (int da = 0; da < 3; ++da)
+#pragma unroll
+      for (int db = 0; db < 3; ++db) {
+        const uint32_t a = min(ax0 + da, ax1), b = min(ay0 + db, ay1);
+        sc[da][db] = dot3_exact(t0, t1, t2, s.dirs + 3 * (a * K + b));
       }
-    }
+#pragma unroll
+    for (int da = 0; da < 3; ++da)
+#pragma unroll
+      for (int db = 0; db < 3; ++db) {
+        const uint32_t a = ax0 + da, b = ay0 + db;
+        if (a <= ax1 && b <= ay1 && sc[da][db] > best) {  // strict: first row-major wins
+          best = sc[da][db];
+          bx = a;
+          by = b;
+        }
+      }
+  } else {
+    for (uint32_t a = ax0; a <= ax1; ++a)
+      for (uint32_t b = ay0; b <= ay1; ++b) {
+        const double sc = dot3_exact(t0, t1, t2, s.dirs + 3 * (a * K + b));
+        if (sc > best) {  // strict: ties keep the first row-major pair
+          best = sc;
+          bx = a;
+          by = b;
+        }
+      }
+  }
   const double cl = best < 0.0 ? 0.0 : (best > 1.0 ? 1.0 : best);
   const uint32_t ir = quantize_lut(s.rb, p.KR - 1, s.rlut, cl, 0.f, 1024.f);
   return bx | (by << 8) | (ir << 16);
