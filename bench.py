@@ -12,7 +12,10 @@ attention, B=8, 28 query / 4 KV heads, d=128, K=V 3-bit (b_dir 4, b_nrm 2),
 whole compressed cache (qprep + fused split-K attention + combine; with N>1
 ranks the cache is sequence-sharded: rank r holds its own 128K-token slice of
 an N*128K context and the partial (m, l, acc) states meet in ONE NCCL
-all-gather, then every rank merges them -> weak scaling).
+all-gather, then every rank merges them -> weak scaling).  The sharded step
+goes through the library's own oq_attention_decode_sharded (fused attention
+writes the rank's partial, ncclAllGather, merge); OQ_BENCH_NCCL=torch uses
+torch.distributed's all-gather instead, OQ_BENCH_SHARDED=1 runs it on one rank.
 value = algorithmic compressed-KV bytes of all ranks (B*Hkv*T*(58+58) B per
 rank) / max-over-ranks step time.  Inputs (486 MB per rank) exceed the 126 MB
 L2, so no flush is needed between steps.
@@ -339,9 +342,21 @@ def main():
     gathered = torch.empty((world * rows, 132), dtype=torch.float32, device=dev)
     out = torch.empty((B, Hq, 128), dtype=torch.float32, device=dev)
 
+    # the sharded step through the library's own NCCL path (fused K3 writes
+    # this rank's partial into the gather buffer, ncclAllGather, merge: one
+    # C call) or through torch.distributed (OQ_BENCH_NCCL=torch)
+    native = sharded and os.environ.get("OQ_BENCH_NCCL", "native") == "native"
+    comm = None
+    if native:
+        uid = [oq.NcclComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = oq.NcclComm(world, uid[0], rank)
+
     def step(qd):
         if not sharded:
             return oq.attention_decode(qd, cache, n_splits=splits, out=out)
+        if native:
+            return oq.attention_decode_sharded(qd, cache, 0, T, comm, n_splits=splits, out=out)
         part = oq.attention_partials(qd, cache, 0, T, n_splits=splits)
         dist.all_gather_into_tensor(gathered, part)
         return oq.attention_combine(cache.enc_v, gathered, rows, world, 132, rows * 132,
@@ -521,6 +536,8 @@ def main():
         print(json.dumps(line), flush=True)
     if sharded:
         dist.barrier()
+        if comm is not None:
+            comm.close()
         dist.destroy_process_group()
     return 0
 
