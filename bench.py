@@ -526,9 +526,9 @@ def main():
                     "what": "pinned q H2D + public-API attention + out D2H per step; KV cache "
                             "device-resident"},
             "clocks": clk.summary(),
-            # world 1: one fused K3 launch per step; sharded: K5 + K3 + local
-            # merge + final merge around the NCCL all-gather
-            "gpu_launches": (4 if sharded else 1) * args.steps,
+            # world 1: one fused K3 launch per step; sharded: the fused K3
+            # (writing this rank's partial) + the merge after the NCCL all-gather
+            "gpu_launches": (2 if sharded else 1) * args.steps,
             "compress": comp,
             "decode_step": step_info,
             "other_configs": others,
