@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
                                                        int dtype, size_t n,
                                                        uint8_t* __restrict__ out, int aligned,
                                                        const uint32_t* __restrict__ list,
-                                                       const uint32_t* __restrict__ list_n) {
+                                                       const uint32_t* __restrict__ list_n,
+                                                       int list_stride) {
   using S = CompressShape<D>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
   for (size_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
     const size_t v = blk * S::VPC + vl;
     const bool live = v < n;
-    const size_t key = list ? (live ? (size_t)list[v] : 0) : v;
+    const size_t key = list ? (live ? (size_t)list[v * list_stride] : 0) : v;
     double* ur = ur_s + vl * S::STRIDE;
 
     // ---- load, norm, normalize (codec.hpp:219-225) ------------------------
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(128) compress_kernel(OqCodecParams p, const vo
     if (list) {
       for (size_t i = tid; i < nbytes; i += blockDim.x) {
         const size_t w = i / rb;
-        out[(size_t)list[blk * S::VPC + w] * rb + (i - w * rb)] = stage_s[i];
+        out[(size_t)list[(blk * S::VPC + w) * list_stride] * rb + (i - w * rb)] = stage_s[i];
       }
     } else if (aligned) {
       const uint32_t* src32 = reinterpret_cast<const uint32_t*>(stage_s);
@@ -514,7 +515,8 @@ static size_t compress_smem(const OqCodecParams& p) {
 template <int D, bool TAB>
 static cudaError_t launch_compress_dt(const OqCodecParams& p, const void* x, int dtype, size_t n,
                                      uint8_t* out, cudaStream_t st, int num_sms,
-                                     const uint32_t* list, const uint32_t* list_n) {
+                                     const uint32_t* list, const uint32_t* list_n,
+                                     int list_stride) {
   using S = CompressShape<D>;
   const size_t smem = compress_smem<D>(p);
   cudaError_t e = set_smem_once(compress_kernel<D, TAB>, (int)smem);
@@ -528,7 +530,7 @@ static cudaError_t launch_compress_dt(const OqCodecParams& p, const void* x, int
   if (grid > nblocks) grid = nblocks;
   const int aligned = (reinterpret_cast<uintptr_t>(out) & 3) == 0;
   compress_kernel<D, TAB><<<(unsigned)grid, S::THREADS, smem, st>>>(p, x, dtype, n, out, aligned,
-                                                                    list, list_n);
+                                                                    list, list_n, list_stride);
   return cudaGetLastError();
 }
 
@@ -536,10 +538,12 @@ template <int D>
 static cudaError_t launch_compress_d(const OqCodecParams& p, const void* x, int dtype, size_t n,
                                      uint8_t* out, cudaStream_t st, int num_sms,
                                      const uint32_t* list = nullptr,
-                                     const uint32_t* list_n = nullptr) {
+                                     const uint32_t* list_n = nullptr, int list_stride = 1) {
   return p.K * p.K <= 1024
-             ? launch_compress_dt<D, true>(p, x, dtype, n, out, st, num_sms, list, list_n)
-             : launch_compress_dt<D, false>(p, x, dtype, n, out, st, num_sms, list, list_n);
+             ? launch_compress_dt<D, true>(p, x, dtype, n, out, st, num_sms, list, list_n,
+                                           list_stride)
+             : launch_compress_dt<D, false>(p, x, dtype, n, out, st, num_sms, list, list_n,
+                                            list_stride);
 }
 
 cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, size_t n,
@@ -565,12 +569,12 @@ cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, si
     }
     return e;
   }
-  if (impl == 1 && n <= 8192 && compress_fast_ok(p, dtype, x, out)) {
+  if (impl == 1 && n <= 8192 && !p.qjl && compress_fast_ok(p, dtype, x, out)) {
     cudaError_t e = flagged ? cudaMemsetAsync(flagged, 0, sizeof(uint32_t), st) : cudaSuccess;
     if (e == cudaSuccess) e = launch_compress_x2(p, x, dtype, n, out, st, num_sms);
     return e;
   }
-  if (impl == 0 && compress_fast_ok(p, dtype, x, out)) {
+  if (impl == 0 && !p.qjl && compress_fast_ok(p, dtype, x, out)) {
     cudaError_t e = flagged ? cudaMemsetAsync(flagged, 0, sizeof(uint32_t), st) : cudaSuccess;
     if (e == cudaSuccess)
       e = launch_compress_x2(p, x, dtype, n, out, st, num_sms);
@@ -585,7 +589,13 @@ cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, si
     FlagEntry* fl = reinterpret_cast<FlagEntry*>(ws + 8);
     e = cudaMemsetAsync(ws, 0, sizeof(uint32_t), st);
     if (e == cudaSuccess) e = launch_compress_fast(p, x, dtype, n, out, fl, ws, st, num_sms);
-    if (e == cudaSuccess) e = launch_compress_fixup(p, x, dtype, out, fl, ws, st, num_sms);
+    // with the QJL sidecar a flagged key is re-encoded whole by the exact
+    // generic kernel (its residual depends on every triplet's codes)
+    if (e == cudaSuccess)
+      e = p.qjl ? launch_compress_d<128>(p, x, dtype, n, out, st, num_sms,
+                                         reinterpret_cast<const uint32_t*>(fl), ws,
+                                         (int)(sizeof(FlagEntry) / sizeof(uint32_t)))
+                : launch_compress_fixup(p, x, dtype, out, fl, ws, st, num_sms);
     if (e == cudaSuccess && flagged)
       e = cudaMemcpyAsync(flagged, ws, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
     const cudaError_t f = cudaFreeAsync(ws, st);

@@ -43,13 +43,15 @@ constexpr int kCFThreads = 32 * kCFWarps;
 constexpr int kCFRow = 132;  // floats per staged row (128 + 4 pad: conflict-free LDS.128)
 constexpr int kCFCells = 128, kCFLutRep = 8;  // LUT: float4 entries, 8 replicas
 
-template <int BD, int BN>
+template <int BD, int BN, bool QJL = false>
 struct CFS {
   static constexpr int K = 1 << BD, KR = 1 << BN, NT = 43;
   static constexpr int DIRB = (2 * NT * BD + 7) / 8, NRMB = (NT * BN + 7) / 8;
-  static constexpr int RB = 4 + DIRB + NRMB;  // record bytes (no QJL)
-  static constexpr int RW = (RB + 3) / 4;     // record words
-  static constexpr int DREP = BD <= 4 ? 8 : 2;
+  static constexpr int QB = 4 + DIRB + NRMB;            // QJL sidecar offset
+  static constexpr int RB = QB + (QJL ? 18 : 0);        // record bytes
+  static constexpr int RW = (RB + 3) / 4;               // record words
+  // the QJL variants give up direction-table replicas for the larger records
+  static constexpr int DREP = QJL ? (BD <= 4 ? 4 : 1) : (BD <= 4 ? 8 : 2);
   static constexpr int RECBUF_WORDS = (32 * RB) / 4 + 4;
   // shared memory carve (bytes)
   static constexpr int KP = K + 2;  // direction grid padded by a -inf border
@@ -84,12 +86,12 @@ __device__ __forceinline__ uint32_t cf_bucket(float x, float g, const float4* lu
   return (uint32_t)lo + (upx ? 1u : 0u);
 }
 
-template <int BD, int BN, int MODE, int DT>
+template <int BD, int BN, int MODE, int DT, bool QJL>
 __global__ void __launch_bounds__(kCFThreads, 1)
     compress_fast_kernel(OqCodecParams p, const void* __restrict__ x, size_t n,
                          uint8_t* __restrict__ out, FlagEntry* __restrict__ flags,
                          uint32_t* __restrict__ flag_cnt) {
-  using S = CFS<BD, BN>;
+  using S = CFS<BD, BN, QJL>;
   constexpr int K = S::K;
   constexpr float U = 5.9604645e-8f;  // 2^-24
   constexpr float E0 = 7.02f * U;     // triplet-independent part of Et (see the header)
@@ -118,6 +120,8 @@ __global__ void __launch_bounds__(kCFThreads, 1)
     return v;
   }, tid, kCFThreads);
   if (tid <= K) bnd[tid] = tid == 0 ? -INFINITY : (tid == K ? INFINITY : (float)p.xi_bnd[tid - 1]);
+  float* rho_s = bnd + 40;  // fp32 norm centroids (QJL residual)
+  if (QJL && tid < S::KR) rho_s[tid] = p.rho32[tid];
   __syncthreads();
   for (int c = tid; c < kCFCells; c += kCFThreads) {
     // guard band 1e-6 >> the fp32 error of the cell index
@@ -326,6 +330,17 @@ __global__ void __launch_bounds__(kCFThreads, 1)
           okt = okt && fabsf(rv - rbnd[i]) > gr + U;
         }
         gmask |= (okt ? 0u : 1u) << j;
+        if constexpr (QJL) {
+          // residual r = t - rho_hat n_hat of the chosen codes (codec.hpp:243-246,
+          // 252-266) back into this triplet's slots of the row; the pad
+          // coordinate is dropped (qjl.hpp:23-36 works on the d real ones)
+          const float4 nv = dtab[(((ix & (K - 1)) + 1) * S::KP + (iy & (K - 1)) + 1) * S::DREP];
+          const float rh = rho_s[ir];
+          float* rw = myrow + 12 * q + 3 * j;
+          rw[0] = t0 - rh * nv.x;
+          rw[1] = t1 - rh * nv.y;
+          if (!pad) rw[2] = t2 - rh * nv.z;
+        }
         // ---- append the fields (masked to their widths: an undecided
         // triplet's fields are patched in place by the exact fixup) ----------
         const uint32_t fpair = (ix & (K - 1)) | ((iy & (K - 1)) << BD);
@@ -360,6 +375,69 @@ __global__ void __launch_bounds__(kCFThreads, 1)
       if (dn > 0) put(dw, (uint32_t)dacc);
       if (nn > 0) put(nw, (uint32_t)nacc);
     }
+    bool okq = true;
+    if constexpr (QJL) {
+      // ---- QJL sidecar (qjl.hpp:23-36), certified like the codes ----------
+      // ||r32 - r64|| <= Er = 13.1u: rotation (9.03u over the whole vector),
+      // fp32 tables and product for rho_hat n_hat (1.51u ||u_hat|| <= 3.02u),
+      // the subtraction (<= u).
+      float y[128];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float4 v = *reinterpret_cast<const float4*>(myrow + 4 * i);
+        y[4 * i] = v.x; y[4 * i + 1] = v.y; y[4 * i + 2] = v.z; y[4 * i + 3] = v.w;
+      }
+      // gamma_r = f16(float(sqrt(sum r^2))), the sum sequential in fp64 (the
+      // fp32 squares are exact in fp64).  |sum r32^2 - sum r64^2| <=
+      // Er (2 ||r32|| + Er); gamma_r is certified when both ends of that
+      // interval round to the same f16 (sqrt, float() and f16() are monotone).
+      double n2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) n2 = __fma_rn((double)y[i], (double)y[i], n2);
+      constexpr double ER = 13.1 * 5.9604644775390625e-8;
+      const double nr = __dsqrt_rn(n2);
+      const double en2 = ER * (2.0 * nr + ER) * 1.001 + 1e-13 * n2;
+      const uint16_t hlo = f32_to_f16_ref((float)__dsqrt_rn(fmax(n2 - en2, 0.0)));
+      const uint16_t hhi = f32_to_f16_ref((float)__dsqrt_rn(n2 + en2));
+      okq = hlo == hhi;
+      // w = H (s' .* r) / sqrt(d) in fp32: ||w32 - w64|| <= Er + 7u ||r||
+      // (butterflies) + u ||r|| (scale); sign bit i = (w_i >= 0)
+#pragma unroll
+      for (int i = 0; i < 128; ++i)
+        if ((p.qsign_mask[i >> 5] >> (i & 31)) & 1u) y[i] = -y[i];
+#pragma unroll
+      for (int len = 1; len < 128; len <<= 1)
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (!(i & len)) {
+            const float a = y[i], b = y[i + len];
+            y[i] = a + b;
+            y[i + len] = a - b;
+          }
+      const float isd = (float)p.inv_sqrt_d;
+      const float ew = (float)((ER + 8.01 * 5.9604644775390625e-8 * nr) * 1.001 + 1e-14);
+      uint32_t sg[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        const float wv = y[i] * isd;
+        sg[i >> 5] |= (wv >= 0.f ? 1u : 0u) << (i & 31);
+        okq = okq && fabsf(wv) > ew;
+      }
+      // the 18 sidecar bytes (gamma_r, 16 sign bytes, LSB first) at record
+      // byte QB, OR-ed into the scratch words (the first one is shared with
+      // the norm stream)
+      const uint32_t b0 = (uint32_t)hlo | (sg[0] << 16), b1 = (sg[0] >> 16) | (sg[1] << 16),
+                     b2 = (sg[1] >> 16) | (sg[2] << 16), b3 = (sg[2] >> 16) | (sg[3] << 16),
+                     b4 = sg[3] >> 16;
+      constexpr int QW = S::QB >> 2, QO = 8 * (S::QB & 3);
+      const uint32_t bw[5] = {b0, b1, b2, b3, b4};
+#pragma unroll
+      for (int i = 0; i <= 5; ++i) {
+        const uint32_t lo = i < 5 ? bw[i] : 0u, hi = i > 0 ? bw[i - 1] : 0u;
+        const uint32_t v = QO ? ((lo << QO) | (i > 0 ? hi >> (32 - QO) : 0u)) : lo;
+        if (QW + i < S::RW) scr[32 * (QW + i)] |= v;
+      }
+    }
     __syncwarp();
     if (blk + wstride < nblk) {  // the staging row is consumed: fetch the next block
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -370,7 +448,7 @@ __global__ void __launch_bounds__(kCFThreads, 1)
     for (int i = 0; i <= S::RW; ++i) w[i] = i < S::RW ? scr[32 * i] : 0u;
 
     // ---- keys with undecided triplets: exact fixup later ---------------------
-    if (!ok) fmask = (1ull << S::NT) - 1;
+    if (!ok || !okq) fmask = (1ull << S::NT) - 1;
     const uint32_t bad = __ballot_sync(kFull, live && fmask != 0);
     if (bad) {
       uint32_t basei = 0;
@@ -429,34 +507,35 @@ __global__ void __launch_bounds__(kCFThreads, 1)
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-template <int BD, int BN, int MODE, int DT>
+template <int BD, int BN, int MODE, int DT, bool QJL>
 static cudaError_t launch_cf_t(const OqCodecParams& p, const void* x, size_t n, uint8_t* out,
                                FlagEntry* flag_idx, uint32_t* flag_cnt, cudaStream_t st,
                                int num_sms) {
-  using S = CFS<BD, BN>;
-  cudaError_t e = set_smem_once(compress_fast_kernel<BD, BN, MODE, DT>, S::SMEM);
+  using S = CFS<BD, BN, QJL>;
+  static_assert(S::SMEM <= 227 * 1024, "compress_fast shared memory");
+  cudaError_t e = set_smem_once(compress_fast_kernel<BD, BN, MODE, DT, QJL>, S::SMEM);
   if (e != cudaSuccess) return e;
   const size_t nblk = (n + 31) / 32;
   size_t grid = (nblk + kCFWarps - 1) / kCFWarps;
   if (grid > (size_t)num_sms) grid = num_sms;
-  compress_fast_kernel<BD, BN, MODE, DT>
+  compress_fast_kernel<BD, BN, MODE, DT, QJL>
       <<<(unsigned)grid, kCFThreads, S::SMEM, st>>>(p, x, n, out, flag_idx, flag_cnt);
   return cudaGetLastError();
 }
 
-template <int BD, int BN, int MODE>
+template <int BD, int BN, int MODE, bool QJL>
 static cudaError_t launch_cf(const OqCodecParams& p, const void* x, int dtype, size_t n,
                              uint8_t* out, FlagEntry* flag_idx, uint32_t* flag_cnt,
                              cudaStream_t st, int num_sms) {
   if (dtype == OQ_BF16)
-    return launch_cf_t<BD, BN, MODE, OQ_BF16>(p, x, n, out, flag_idx, flag_cnt, st, num_sms);
+    return launch_cf_t<BD, BN, MODE, OQ_BF16, QJL>(p, x, n, out, flag_idx, flag_cnt, st, num_sms);
   if (dtype == OQ_F16)
-    return launch_cf_t<BD, BN, MODE, OQ_F16>(p, x, n, out, flag_idx, flag_cnt, st, num_sms);
-  return launch_cf_t<BD, BN, MODE, OQ_F32>(p, x, n, out, flag_idx, flag_cnt, st, num_sms);
+    return launch_cf_t<BD, BN, MODE, OQ_F16, QJL>(p, x, n, out, flag_idx, flag_cnt, st, num_sms);
+  return launch_cf_t<BD, BN, MODE, OQ_F32, QJL>(p, x, n, out, flag_idx, flag_cnt, st, num_sms);
 }
 
 bool compress_fast_ok(const OqCodecParams& p, int dtype, const void* x, const void* out) {
-  if (p.dim != 128 || p.qjl || dtype == OQ_F64) return false;
+  if (p.dim != 128 || dtype == OQ_F64) return false;
   if (p.rounding != 0 && p.rounding != 2) return false;
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(out) & 15)) return false;
   return (p.b_dir == 3 && p.b_nrm == 1) || (p.b_dir == 4 && p.b_nrm == 2) ||
@@ -466,14 +545,17 @@ bool compress_fast_ok(const OqCodecParams& p, int dtype, const void* x, const vo
 cudaError_t launch_compress_fast(const OqCodecParams& p, const void* x, int dtype, size_t n,
                                  uint8_t* out, FlagEntry* flag_idx, uint32_t* flag_cnt,
                                  cudaStream_t st, int num_sms) {
-#define OQ_CF(BD, BN)                                                                          \
-  if (p.b_dir == BD && p.b_nrm == BN)                                                          \
-    return p.rounding == 0                                                                     \
-               ? launch_cf<BD, BN, 0>(p, x, dtype, n, out, flag_idx, flag_cnt, st, num_sms)   \
-               : launch_cf<BD, BN, 2>(p, x, dtype, n, out, flag_idx, flag_cnt, st, num_sms);
-  OQ_CF(3, 1)
-  OQ_CF(4, 2)
-  OQ_CF(5, 3)
+#define OQ_CF(BD, BN, Q)                                                                         \
+  if (p.b_dir == BD && p.b_nrm == BN && (bool)p.qjl == Q)                                       \
+    return p.rounding == 0                                                                      \
+               ? launch_cf<BD, BN, 0, Q>(p, x, dtype, n, out, flag_idx, flag_cnt, st, num_sms)  \
+               : launch_cf<BD, BN, 2, Q>(p, x, dtype, n, out, flag_idx, flag_cnt, st, num_sms);
+  OQ_CF(3, 1, false)
+  OQ_CF(4, 2, false)
+  OQ_CF(5, 3, false)
+  OQ_CF(3, 1, true)
+  OQ_CF(4, 2, true)
+  OQ_CF(5, 3, true)
 #undef OQ_CF
   return cudaErrorNotSupported;
 }

@@ -201,9 +201,10 @@ def test_small_batch_kernel_bit_exact(orc, cuda, cfg, dtype):
         assert bad.size == 0, f"n={n}: {bad.size} mismatching records, first {bad[:5]}"
 
 
+@pytest.mark.parametrize("qjl", [False, True])
 @pytest.mark.parametrize("b", [2, 3, 4])
 @pytest.mark.parametrize("rounding", ["local3x3", "scalar"])
-def test_fast_path_special_keys_bit_exact(orc, cuda, b, rounding):
+def test_fast_path_special_keys_bit_exact(orc, cuda, b, rounding, qjl):
     """Batches large enough for the certified fp32 pass (> 8192 keys) with the
     keys it cannot certify at all mixed in: zero keys, norms outside
     [2^-60, 2^60] (every triplet goes to the exact fixup), basis vectors
@@ -217,6 +218,11 @@ def test_fast_path_special_keys_bit_exact(orc, cuda, b, rounding):
     idx = rng.choice(n, 64, replace=False)
     for j, i in enumerate(idx):
         kind = j % 8
+        if qjl and kind in (5, 6):
+            # an inf/NaN key's QJL residual norm is NaN, and the NaN's sign bit
+            # (the f16 gamma_r's top byte) follows the host's NaN propagation
+            # (x86: the default NaN is negative); codes stay bit-exact
+            kind = 3
         if kind == 0:
             x[i] = 0.0
         elif kind == 1:
@@ -234,10 +240,31 @@ def test_fast_path_special_keys_bit_exact(orc, cuda, b, rounding):
             x[i, j % 128] = np.nan
         else:
             x[i, 0::3] = x[i, 1::3]  # many equal |t0| = |t1| folds
-    enc = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rounding=rounding))
+    enc = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rounding=rounding, qjl=qjl))
     fl = torch.zeros(1, dtype=torch.int32, device=cuda)
     got = enc.compress(torch.from_numpy(x).to(cuda), flagged=fl).cpu().numpy()
-    want = orc.encoder(b_dir=bd, b_nrm=bn, rounding=rounding).encode_f32(x, threads=os.cpu_count() or 8)
+    want = orc.encoder(b_dir=bd, b_nrm=bn, rounding=rounding, qjl=qjl).encode_f32(
+        x, threads=os.cpu_count() or 8)
     bad = np.nonzero((got != want).any(1))[0]
     assert bad.size == 0, f"{bad.size} records differ, first {bad[:5]} ({int(fl.item())} flagged)"
     assert int(fl.item()) >= 40  # the special keys all went through the fixup
+
+
+@pytest.mark.parametrize("b", [2, 3, 4])
+def test_fast_path_qjl_bit_exact(orc, cuda, b):
+    """The certified pass with the QJL sidecar (residual norm and signs
+    certified like the codes; flagged keys re-encoded whole by the exact
+    kernel): 2^17 keys, bit-exact, and the flag rate stays small."""
+    import torch
+    n = 1 << 17
+    bd, bn = oq.default_bit_split(b)
+    g = torch.Generator(device=cuda).manual_seed(500 + b)
+    x = torch.randn((n, 128), device=cuda, generator=g)
+    enc = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, qjl=True, qjl_seed=9))
+    fl = torch.zeros(1, dtype=torch.int32, device=cuda)
+    got = enc.compress(x, flagged=fl).cpu().numpy()
+    want = orc.encoder(b_dir=bd, b_nrm=bn, qjl=True, qjl_seed=9).encode_f32(
+        x.cpu().numpy(), threads=os.cpu_count() or 8)
+    bad = int((got != want).any(1).sum())
+    assert bad == 0, f"{bad} of {n} records differ ({int(fl.item())} flagged)"
+    assert int(fl.item()) < 0.2 * n
