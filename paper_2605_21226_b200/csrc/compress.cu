@@ -549,10 +549,13 @@ static cudaError_t launch_compress_d(const OqCodecParams& p, const void* x, int 
 cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, size_t n,
                             uint8_t* out, cudaStream_t st, int num_sms, uint32_t* flagged) {
   if (n == 0) return cudaSuccess;
-  // d = 128 fp32 keys at the BASELINE bit splits: the single-pass two-lanes-
-  // per-key kernel (compress_x2.cu) unless OQ_COMPRESS_IMPL selects the
-  // certified-fp32 pass + exact re-encode ("fast") or the generic exact
-  // kernel ("exact") for comparison runs.
+  // d = 128 fp32 / fp16 / bf16 keys at the BASELINE bit splits (scalar or
+  // local3x3): up to 2048 keys one warp per key (exact), up to 8192 the
+  // single-pass two-lanes-per-key kernel (compress_x2.cu), beyond that the
+  // certified fp32 pass + the exact fixup of its undecided triplets (or, with
+  // QJL, of its flagged keys).  Every other config: the generic exact kernel.
+  // OQ_COMPRESS_IMPL=x (x2 only) / e (generic only) select a kernel for
+  // comparison runs.
   static const int impl = [] {
     const char* e = getenv("OQ_COMPRESS_IMPL");
     if (!e) return 1;
