@@ -699,14 +699,25 @@ __device__ __forceinline__ void combine_row(const float* base, int n, float* out
 #pragma unroll
   for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
   float L = 0.f, y[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int i = 0; i < n; ++i) {
-    const float2 ml = *reinterpret_cast<const float2*>(base + (size_t)i * kPartW);
-    if (ml.y > 0.f) {
-      const float f = ex2(ml.x - M);
-      L += ml.y * f;
-      const float4 a4 = *reinterpret_cast<const float4*>(base + (size_t)i * kPartW + 4 + 4 * lane);
-      y[0] += a4.x * f; y[1] += a4.y * f; y[2] += a4.z * f; y[3] += a4.w * f;
+  // the parts were just written by other CTAs (L2): request a batch of them
+  // before consuming it, instead of one dependent round trip per part
+  constexpr int NB = 4;
+  for (int i0 = 0; i0 < n; i0 += NB) {
+    float2 ml[NB];
+    float4 a4[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {  // past the end: re-read the last part, skipped below
+      const size_t i = (size_t)min(i0 + j, n - 1);
+      ml[j] = *reinterpret_cast<const float2*>(base + i * kPartW);
+      a4[j] = *reinterpret_cast<const float4*>(base + i * kPartW + 4 + 4 * lane);
     }
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (i0 + j < n && ml[j].y > 0.f) {  // in part order, as before
+        const float f = ex2(ml[j].x - M);
+        L += ml[j].y * f;
+        y[0] += a4[j].x * f; y[1] += a4[j].y * f; y[2] += a4[j].z * f; y[3] += a4[j].w * f;
+      }
   }
   if (partial) {
     if (lane == 0) *reinterpret_cast<float4*>(out) = make_float4(M, L, 0.f, 0.f);
