@@ -592,29 +592,39 @@ __device__ __forceinline__ void warp_state_out(WarpState& S, float* mw, int g, i
 }
 
 // CTA merge of NW warp states (SoftmaxState::merge, attention.hpp:36-44) and
-// the segment's partial store; threads [0, nthreads) participate.
+// the segment's partial store; threads [0, nthreads) participate.  The
+// per-(warp, head) scale factors are computed once (mf: NW + 1 rows of 8
+// floats of shared scratch; row NW holds the merged maxima), then every
+// element is a dot product over the warps.
 template <int NW>
 __device__ __forceinline__ void merge_store(const AttnKParams& P, const Seg& it,
-                                            const float* merge, int tid, int nthreads) {
+                                            const float* merge, float* mf, int tid,
+                                            int nthreads) {
   const float NEG_INF = -__int_as_float(0x7f800000);
   const int nh = min(8, P.G - 8 * it.hc);
-  for (int idx = tid; idx < nh * kPartW; idx += nthreads) {
-    const int h = idx / kPartW, j = idx % kPartW;
+  if (tid < nh) {
     float M = NEG_INF;
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
-      const float* mm = merge + (w * 8 + h) * kPartW;
+      const float* mm = merge + (w * 8 + tid) * kPartW;
       if (mm[1] > 0.f) M = fmaxf(M, mm[0]);
     }
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const float* mm = merge + (w * 8 + tid) * kPartW;
+      mf[w * 8 + tid] = mm[1] > 0.f ? ex2(mm[0] - M) : 0.f;
+    }
+    mf[NW * 8 + tid] = M;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < nh * kPartW; idx += nthreads) {
+    const int h = idx / kPartW, j = idx % kPartW;
     float v = 0.f;
     if (j == 0) {
-      v = M;
+      v = mf[NW * 8 + h];
     } else if (j == 1 || j >= 4) {
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const float* mm = merge + (w * 8 + h) * kPartW;
-        if (mm[1] > 0.f) v += mm[j] * ex2(mm[0] - M);
-      }
+      for (int w = 0; w < NW; ++w) v += merge[(w * 8 + h) * kPartW + j] * mf[w * 8 + h];
     }
     const size_t row = (size_t)it.b * P.Hq + (size_t)it.kvh * P.G + 8 * it.hc + h;
     P.partials[(row * P.n_parts + it.part) * kPartW + j] = v;
@@ -748,6 +758,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
   float* merge = reinterpret_cast<float*>(smem + C::TAB_BYTES);
   float* qs = merge + kAttnWarps * 8 * kPartW;
   __shared__ int s_last;
+  __shared__ float s_mf[(kAttnWarps + 1) * 8];  // merge_store scale factors
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, c = lane & 3;
 
@@ -788,7 +799,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
     }
     warp_state_out(S, merge + warp * 8 * kPartW, g, c);
     __syncthreads();
-    merge_store<kAttnWarps>(P, it, merge, tid, blockDim.x);
+    merge_store<kAttnWarps>(P, it, merge, s_mf, tid, blockDim.x);
     if (P.fuse) {
       // the CTA that lands a stream's last partial finalises its rows
       __threadfence();
