@@ -175,8 +175,11 @@ __device__ __forceinline__ void stage_table(uint2* dst, const uint2* __restrict_
       if (e < NE) {
         uint4* d = reinterpret_cast<uint4*>(dst + (size_t)e * REP);
         const uint4 q = make_uint4(v[k].x, v[k].y, v[k].x, v[k].y);
+        // consecutive lanes write consecutive entries (a multiple of 128 B
+        // apart): rotate the slot order by lane so that a store instruction's
+        // eight-lane phases hit eight different bank groups
 #pragma unroll
-        for (int r = 0; r < REP / 2; ++r) d[r] = q;
+        for (int r = 0; r < REP / 2; ++r) d[(r + tid) & (REP / 2 - 1)] = q;
       }
     }
   }
