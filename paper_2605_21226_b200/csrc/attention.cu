@@ -257,6 +257,7 @@ struct AttnKParams {
   // [tb0, tb0 + tps) are cut into gridDim.x equal contiguous ranges.
   int streamk, n_sh;
   size_t tb0, tps;
+  size_t sko;  // stream-K: per-stream segment overhead in tile units
   // fused mode (single-GPU attention_decode): the kernel prepares the query
   // fragments itself from q and finalises each stream's rows once its last
   // partial lands (per-stream arrival counters, left at zero)
@@ -831,13 +832,17 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
     for (int item = blockIdx.x; item < P.n_items; item += gridDim.x)
       run(item_seg(P, item), P.splits);
   } else {
-    const size_t U = (size_t)P.n_sh * P.tps, G = gridDim.x;
+    // stream-K over virtual units: each stream is sko units of segment
+    // overhead (q prep, pipeline restart, merge) followed by its tps tiles,
+    // so a CTA that starts a second stream gets correspondingly fewer tiles
+    const size_t V = P.tps + P.sko, U = (size_t)P.n_sh * V, G = gridDim.x;
     const size_t u0 = sk_bound(blockIdx.x, U, G), u1 = sk_bound(blockIdx.x + 1, U, G);
-    for (size_t sh = u0 / P.tps; sh * P.tps < u1; ++sh) {
-      const size_t s0 = sh * P.tps, s1 = s0 + P.tps;
-      const size_t a = max(u0, s0), z = min(u1, s1);
-      const int first = sk_cta(s0, U, G), part = (int)blockIdx.x - first;
-      run(make_seg(P, (int)sh, P.tb0 + (a - s0), P.tb0 + (z - s0), part, z == s1),
+    for (size_t sh = u0 / V; sh * V < u1; ++sh) {
+      const size_t t0 = sh * V + P.sko, s1 = sh * V + V;  // the stream's tile units
+      const size_t a = max(u0, t0), z = min(u1, s1);
+      if (a >= z) continue;  // only overhead units of this stream
+      const int first = sk_cta(t0, U, G), part = (int)blockIdx.x - first;
+      run(make_seg(P, (int)sh, P.tb0 + (a - t0), P.tb0 + (z - t0), part, z == s1),
           sk_cta(s1 - 1, U, G) - first + 1);
     }
   }
@@ -1373,6 +1378,14 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
     P.vmask[i] = a.vmask[i];
   }
   P.inv_sqrt_d = (float)pk.inv_sqrt_d;
+  {
+    // a stream start costs about as much as this many tiles on one SM
+    static const long sko_env = [] {
+      const char* e = getenv("OQ_ATTN_SKO");
+      return e ? atol(e) : -1L;
+    }();
+    P.sko = sko_env >= 0 ? (size_t)sko_env : (P.tps >= 512 ? 32 : 0);
+  }
   int grid = P.n_items < num_sms ? P.n_items : num_sms;
   if (P.streamk) {
     const size_t U = (size_t)P.n_sh * P.tps;
