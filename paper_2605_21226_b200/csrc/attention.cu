@@ -832,17 +832,23 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
     __syncthreads();
     merge_store<kAttnWarps>(P, it, merge, s_mf, tid, blockDim.x);
     if (P.fuse) {
-      // the CTA that lands a stream's last partial finalises its rows
-      __threadfence();
+      // the CTA that lands a stream's last partial finalises its rows.  The
+      // barrier orders the CTA's partial stores before thread 0's gpu-scope
+      // acq_rel arrival (release cumulativity); the CTA that arrives last
+      // acquires every other CTA's partials through the same counter, and
+      // the second barrier passes that on to its threads.
       __syncthreads();
       if (tid == 0) {
-        const uint32_t old = atomicAdd(&P.counters[it.sh], 1u);
+        uint32_t old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                     : "=r"(old)
+                     : "l"(P.counters + it.sh)
+                     : "memory");
         s_last = old + 1 == (uint32_t)nparts;
         if (s_last) P.counters[it.sh] = 0u;
       }
       __syncthreads();
       if (s_last) {
-        __threadfence();
         for (int w = warp; w < 8; w += kAttnWarps) {
           if (8 * it.hc + w >= P.G) continue;
           const size_t row = (size_t)it.b * P.Hq + (size_t)it.kvh * P.G + 8 * it.hc + w;
