@@ -185,23 +185,9 @@ __global__ void __launch_bounds__(kCFThreads, 1)
     load_elems<DT, 128>(y, myrow);  // exact widening of fp16 / bf16 keys
     const bool live = lane < nk;
 
-    // ---- gamma: sequential fp64 sum of squares (codec.hpp:219-221) -----------
-    double g2 = 0.0;
-#pragma unroll
-    for (int i = 0; i < 128; ++i) {
-      const double d = (double)y[i];
-      g2 = __fma_rn(d, d, g2);  // the square is exact: == g2 + d*d rounded once
-    }
-    const double gamma = __dsqrt_rn(g2);
-    const float gf = (float)gamma;  // codec.hpp:233
-    const double inv = __ddiv_rn(1.0, gamma > 1e-12 ? gamma : 1e-12);
-    const float c32 = (float)(inv * p.inv_sqrt_d);
-    // outside [2^-60, 2^60] the fp32 rotation could lose range: exact path
-    // for every triplet
-    const bool ok = gamma > 8.7e-19 && gamma < 1.1e18;
-    uint64_t fmask = 0;  // triplets whose decisions missed their margins
-
     // ---- rotation in fp32: ur = H (s .* k) * c -------------------------------
+    // (the unscaled signs + WHT first: gamma's serial fp64 chain below reads
+    // the untouched staging row, so the two interleave)
 #pragma unroll
     for (int i = 0; i < 128; ++i)
       if ((p.sign_mask[i >> 5] >> (i & 31)) & 1u) y[i] = -y[i];
@@ -214,6 +200,34 @@ __global__ void __launch_bounds__(kCFThreads, 1)
           y[i] = a + b;
           y[i + len] = a - b;
         }
+
+    // ---- gamma: sequential fp64 sum of squares (codec.hpp:219-221) -----------
+    double g2 = 0.0;
+#pragma unroll
+    for (int i4 = 0; i4 < 32; ++i4) {
+      float k4[4];
+      if constexpr (DT == OQ_F32) {
+        const float4 v = reinterpret_cast<const float4*>(myrow)[i4];
+        k4[0] = v.x; k4[1] = v.y; k4[2] = v.z; k4[3] = v.w;
+      } else {
+        const uint2 v = reinterpret_cast<const uint2*>(myrow)[i4];
+        k4[0] = widen16<DT>(v.x & 0xffffu); k4[1] = widen16<DT>(v.x >> 16);
+        k4[2] = widen16<DT>(v.y & 0xffffu); k4[3] = widen16<DT>(v.y >> 16);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double d = (double)k4[j];
+        g2 = __fma_rn(d, d, g2);  // the square is exact: == g2 + d*d rounded once
+      }
+    }
+    const double gamma = __dsqrt_rn(g2);
+    const float gf = (float)gamma;  // codec.hpp:233
+    const double inv = __ddiv_rn(1.0, gamma > 1e-12 ? gamma : 1e-12);
+    const float c32 = (float)(inv * p.inv_sqrt_d);
+    // outside [2^-60, 2^60] the fp32 rotation could lose range: exact path
+    // for every triplet
+    const bool ok = gamma > 8.7e-19 && gamma < 1.1e18;
+    uint64_t fmask = 0;  // triplets whose decisions missed their margins
 #pragma unroll
     for (int i = 0; i < 128; ++i) y[i] *= c32;
 
