@@ -405,17 +405,10 @@ __global__ void __launch_bounds__(kCFThreads, 1)
       // fp32 squares are exact in fp64).  |sum r32^2 - sum r64^2| <=
       // Er (2 ||r32|| + Er); gamma_r is certified when both ends of that
       // interval round to the same f16 (sqrt, float() and f16() are monotone).
-      double n2 = 0.0;
-#pragma unroll
-      for (int i = 0; i < 128; ++i) n2 = __fma_rn((double)y[i], (double)y[i], n2);
-      constexpr double ER = 13.1 * 5.9604644775390625e-8;
-      const double nr = __dsqrt_rn(n2);
-      const double en2 = ER * (2.0 * nr + ER) * 1.001 + 1e-13 * n2;
-      const uint16_t hlo = f32_to_f16_ref((float)__dsqrt_rn(fmax(n2 - en2, 0.0)));
-      const uint16_t hhi = f32_to_f16_ref((float)__dsqrt_rn(n2 + en2));
-      okq = hlo == hhi;
       // w = H (s' .* r) / sqrt(d) in fp32: ||w32 - w64|| <= Er + 7u ||r||
-      // (butterflies) + u ||r|| (scale); sign bit i = (w_i >= 0)
+      // (butterflies) + u ||r|| (scale); sign bit i = (w_i >= 0).  The
+      // butterflies first: the serial n2 chain reads the row in shared memory
+      // and interleaves with them.
 #pragma unroll
       for (int i = 0; i < 128; ++i)
         if ((p.qsign_mask[i >> 5] >> (i & 31)) & 1u) y[i] = -y[i];
@@ -428,6 +421,21 @@ __global__ void __launch_bounds__(kCFThreads, 1)
             y[i] = a + b;
             y[i + len] = a - b;
           }
+      double n2 = 0.0;
+#pragma unroll
+      for (int i4 = 0; i4 < 32; ++i4) {
+        const float4 v = *reinterpret_cast<const float4*>(myrow + 4 * i4);
+        n2 = __fma_rn((double)v.x, (double)v.x, n2);
+        n2 = __fma_rn((double)v.y, (double)v.y, n2);
+        n2 = __fma_rn((double)v.z, (double)v.z, n2);
+        n2 = __fma_rn((double)v.w, (double)v.w, n2);
+      }
+      constexpr double ER = 13.1 * 5.9604644775390625e-8;
+      const double nr = __dsqrt_rn(n2);
+      const double en2 = ER * (2.0 * nr + ER) * 1.001 + 1e-13 * n2;
+      const uint16_t hlo = f32_to_f16_ref((float)__dsqrt_rn(fmax(n2 - en2, 0.0)));
+      const uint16_t hhi = f32_to_f16_ref((float)__dsqrt_rn(n2 + en2));
+      okq = hlo == hhi;
       const float isd = (float)p.inv_sqrt_d;
       const float ew = (float)((ER + 8.01 * 5.9604644775390625e-8 * nr) * 1.001 + 1e-14);
       uint32_t sg[4] = {0u, 0u, 0u, 0u};
