@@ -137,9 +137,8 @@ oq_status oq_cache_append(const oq_codec* codec, int role, const void* x, int dt
                           void* tiles, uint64_t cap_tokens, void* stream);
 /* Decode step, K and V together: encode k and v (device [n_streams][dim]) and
  * write them at token pos of every stream (as oq_cache_append).  For d = 128
- * without QJL this is ONE kernel launch (each warp encodes its stream's
- * vector exactly into shared memory and writes it into the tile); QJL keys
- * take oq_cache_append per role.  k_records / v_records: optional device
+ * this is ONE kernel launch (each warp encodes its stream's vector exactly,
+ * QJL sidecar included, into shared memory and writes it into the tile).  k_records / v_records: optional device
  * outputs for the OCTO records (NULL: not written). */
 oq_status oq_cache_append_kv(const oq_codec* ck, const oq_codec* cv, const void* k, const void* v,
                              int dtype, uint64_t n_streams, const int64_t* pos_dev, int64_t pos,

@@ -1256,7 +1256,8 @@ __global__ void __launch_bounds__(256) append_token_kernel(
 // Fused decode-step append of K AND V (oq_cache_append_kv): blockIdx.y is the
 // role; each warp encodes its stream's new vector (encode_key_warp, exact)
 // straight into shared memory and writes it into the tile — one launch per
-// step instead of compress + append for each of K and V.  d = 128, no QJL.
+// step instead of compress + append for each of K and V.  d = 128 (QJL keys
+// included: qjl_key_warp adds the sidecar).
 constexpr int kAppendWarps = 4;
 __global__ void __launch_bounds__(32 * kAppendWarps) append_fused_kernel(
     const __grid_constant__ OqCodecParams pk, const __grid_constant__ OqCodecParams pv,
@@ -1294,6 +1295,7 @@ __global__ void __launch_bounds__(32 * kAppendWarps) append_fused_kernel(
   }
   append_stage_runs(p, role, s, pos, tiles, tiles_cap, run_s[wib], lane);
   encode_key_warp(p, role ? xv : xk, dtype, s, row_s[wib], rec_s[wib], lane);
+  if (p.qjl) qjl_key_warp(p, row_s[wib], rec_s[wib], lane, global_tables(p));
   uint8_t* recs = role ? rv : rk;
   if (recs) {
     const uint8_t* src = reinterpret_cast<const uint8_t*>(rec_s[wib]);

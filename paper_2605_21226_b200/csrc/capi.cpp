@@ -496,7 +496,7 @@ oq_status oq_cache_append_kv(const oq_codec* ck, const oq_codec* cv, const void*
     return fail(OQ_ERR_INVALID_ARGUMENT, "bad dtype");
   if (n_streams == 0) return OQ_OK;
   cudaStream_t st = as_stream(stream);
-  if (!ck->cfg.qjl) {  // one launch: both roles encoded and written in place
+  if (ck->cfg.dim == 128) {  // one launch: both roles encoded and written in place
     cudaError_t e = oqd::launch_append_fused(
         ck->p, cv->p, k, v, dtype, n_streams, pos_dev, pos, static_cast<uint8_t*>(k_records),
         static_cast<uint8_t*>(v_records), static_cast<uint8_t*>(ktiles),

@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps) compress_small_kernel(
   const size_t key = blockIdx.x * (size_t)kSmallWarps + wib;
   if (key >= n) return;
   encode_key_warp(p, x, dtype, key, row_s[wib], rec_s[wib], lane);
+  if (p.qjl) qjl_key_warp(p, row_s[wib], rec_s[wib], lane, global_tables(p));
   const uint32_t rb = p.rec_bytes;
   uint8_t* dst = out + key * rb;
   const uint8_t* src = reinterpret_cast<const uint8_t*>(rec_s[wib]);
@@ -498,6 +499,28 @@ cudaError_t launch_compress_fixup(const OqCodecParams& p, const void* x, int dty
   return cudaGetLastError();
 }
 
+// Whole-key exact re-encode of the keys the certified pass flagged, one warp
+// per key (used with the QJL sidecar, whose residual depends on every code).
+__global__ void __launch_bounds__(32 * kSmallWarps) compress_rekey_kernel(
+    OqCodecParams p, const void* __restrict__ x, int dtype, uint8_t* __restrict__ out,
+    const FlagEntry* __restrict__ flags, const uint32_t* __restrict__ flag_cnt) {
+  __shared__ double row_s[kSmallWarps][132];
+  __shared__ uint32_t rec_s[kSmallWarps][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t n = *flag_cnt;
+  const uint32_t rb = p.rec_bytes;
+  for (size_t i = blockIdx.x * (size_t)kSmallWarps + wib; i < n;
+       i += (size_t)gridDim.x * kSmallWarps) {
+    const size_t key = flags[i].key;
+    encode_key_warp(p, x, dtype, key, row_s[wib], rec_s[wib], lane);
+    if (p.qjl) qjl_key_warp(p, row_s[wib], rec_s[wib], lane, global_tables(p));
+    uint8_t* dst = out + key * rb;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(rec_s[wib]);
+    for (uint32_t b = lane; b < rb; b += 32) dst[b] = src[b];
+    __syncwarp();
+  }
+}
+
 template <int D>
 static size_t compress_smem(const OqCodecParams& p) {
   using S = CompressShape<D>;
@@ -563,7 +586,7 @@ cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, si
   }();
   // small batches (a decode step appends B*Hkv keys): one warp per key,
   // exact, one launch, no table staging
-  if (impl == 1 && n <= 2048 && p.dim == 128 && !p.qjl) {
+  if (impl == 1 && n <= 2048 && p.dim == 128) {
     cudaError_t e = flagged ? cudaMemsetAsync(flagged, 0, sizeof(uint32_t), st) : cudaSuccess;
     if (e == cudaSuccess) {
       compress_small_kernel<<<(unsigned)((n + kSmallWarps - 1) / kSmallWarps), 32 * kSmallWarps, 0,
@@ -592,13 +615,16 @@ cudaError_t launch_compress(const OqCodecParams& p, const void* x, int dtype, si
     FlagEntry* fl = reinterpret_cast<FlagEntry*>(ws + 8);
     e = cudaMemsetAsync(ws, 0, sizeof(uint32_t), st);
     if (e == cudaSuccess) e = launch_compress_fast(p, x, dtype, n, out, fl, ws, st, num_sms);
-    // with the QJL sidecar a flagged key is re-encoded whole by the exact
-    // generic kernel (its residual depends on every triplet's codes)
-    if (e == cudaSuccess)
-      e = p.qjl ? launch_compress_d<128>(p, x, dtype, n, out, st, num_sms,
-                                         reinterpret_cast<const uint32_t*>(fl), ws,
-                                         (int)(sizeof(FlagEntry) / sizeof(uint32_t)))
-                : launch_compress_fixup(p, x, dtype, out, fl, ws, st, num_sms);
+    // with the QJL sidecar a flagged key is re-encoded whole, one warp per
+    // key (its residual depends on every triplet's codes)
+    if (e == cudaSuccess) {
+      if (p.qjl) {
+        compress_rekey_kernel<<<num_sms * 16, 32 * kSmallWarps, 0, st>>>(p, x, dtype, out, fl, ws);
+        e = cudaGetLastError();
+      } else {
+        e = launch_compress_fixup(p, x, dtype, out, fl, ws, st, num_sms);
+      }
+    }
     if (e == cudaSuccess && flagged)
       e = cudaMemcpyAsync(flagged, ws, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
     const cudaError_t f = cudaFreeAsync(ws, st);

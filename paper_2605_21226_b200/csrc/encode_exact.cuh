@@ -174,10 +174,11 @@ __device__ __forceinline__ uint32_t joint_round(const OqCodecParams& p, const Co
 // 1/sqrt(d) -> row[0 .. 129) (row[128] = 0, the pad).  Lane l holds
 // coordinates 4l .. 4l+3.  Ends with a __syncwarp.
 __device__ __forceinline__ void rotate_key_warp(const OqCodecParams& p, const double (&k)[4],
-                                                double inv, double* row, int lane) {
+                                                double inv, double* row, int lane,
+                                                const uint32_t* mask = nullptr) {
   double v[4];
   // u = k * inv, signs, fwht (rotation.hpp:20-31, 46-49)
-  const uint32_t sm = p.sign_mask[lane >> 3] >> (4 * (lane & 7));
+  const uint32_t sm = (mask ? mask : p.sign_mask)[lane >> 3] >> (4 * (lane & 7));
 #pragma unroll
   for (int i = 0; i < 4; ++i) v[i] = dflip(dmul(k[i], inv), (sm >> i) & 1u);
   {
@@ -252,6 +253,53 @@ __device__ __forceinline__ void encode_key_warp(const OqCodecParams& p, const vo
   }
   __syncwarp();
   if (lane == 0) rec[0] = __float_as_uint((float)gamma);  // codec.hpp:233
+  __syncwarp();
+}
+
+// The QJL sidecar (codec.hpp:243-247, qjl.hpp:23-36) of a key encoded by
+// encode_key_warp: its codes are in rec, its reference rotated coordinates in
+// row[0 .. 127].  r = ur - rho_hat n_hat (reconstruct_rotated, fp64, in place
+// over row), gamma_r = f16(float(sqrt(sum r^2))) with the reference's
+// sequential fp64 sum, w = R' r (signs of qjl_seed, WHT, 1/sqrt d); sign bit
+// i = (w_i >= 0).  Ends with a __syncwarp.
+__device__ __forceinline__ uint32_t rec_bits_w(const uint32_t* w, int pos, int bits) {
+  const int i = pos >> 5, sh = pos & 31;
+  const uint32_t v = sh + bits > 32 ? __funnelshift_r(w[i], w[i + 1], sh) : w[i] >> sh;
+  return v & ((1u << bits) - 1u);
+}
+__device__ __forceinline__ void qjl_key_warp(const OqCodecParams& p, double* row, uint32_t* rec,
+                                             int lane, const CompressSmem& tabs) {
+  const int K = (int)p.K, bd = (int)p.b_dir, bn = (int)p.b_nrm;
+  double r[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int i = 4 * lane + j, t = i / 3, comp = i - 3 * t;
+    const uint32_t pr = rec_bits_w(rec, 32 + 2 * bd * t, 2 * bd);
+    const uint32_t ir = rec_bits_w(rec, 32 + 8 * (int)p.dir_bytes + bn * t, bn);
+    const uint32_t a = pr & (uint32_t)(K - 1), b = pr >> bd;
+    const double uh = dmul(tabs.rc[ir], tabs.dirs[3 * (a * (uint32_t)K + b) + comp]);
+    r[j] = dsub(row[i], uh);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) row[4 * lane + j] = r[j];
+  __syncwarp();
+  double n2 = 0.0;
+  if (lane == 0)
+    for (int i = 0; i < 128; ++i) n2 = dadd(n2, dmul(row[i], row[i]));
+  __syncwarp();
+  rotate_key_warp(p, r, 1.0, row, lane, p.qsign_mask);  // w (r * 1.0 is exact)
+  const int qb = 8 * (4 + (int)p.dir_bytes + (int)p.nrm_bytes);  // sidecar bit offset
+  uint32_t bits = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) bits |= (row[4 * lane + j] >= 0.0 ? 1u : 0u) << j;
+  const int sp = qb + 16 + 4 * lane;  // sign bits LSB-first after gamma_r
+  atomicOr(&rec[sp >> 5], bits << (sp & 31));
+  if (lane == 0) {
+    const uint32_t gr = f32_to_f16_ref((float)dsqrt(n2));
+    atomicOr(&rec[qb >> 5], gr << (qb & 31));
+    if ((qb & 31) > 16) atomicOr(&rec[(qb >> 5) + 1], gr >> (32 - (qb & 31)));
+  }
   __syncwarp();
 }
 
