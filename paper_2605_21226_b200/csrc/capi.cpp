@@ -496,28 +496,13 @@ oq_status oq_cache_append_kv(const oq_codec* ck, const oq_codec* cv, const void*
     return fail(OQ_ERR_INVALID_ARGUMENT, "bad dtype");
   if (n_streams == 0) return OQ_OK;
   cudaStream_t st = as_stream(stream);
-  if (ck->cfg.dim == 128) {  // one launch: both roles encoded and written in place
-    cudaError_t e = oqd::launch_append_fused(
-        ck->p, cv->p, k, v, dtype, n_streams, pos_dev, pos, static_cast<uint8_t*>(k_records),
-        static_cast<uint8_t*>(v_records), static_cast<uint8_t*>(ktiles),
-        static_cast<uint8_t*>(vtiles), (cap_tokens + 31) / 32, st);
-    return e == cudaSuccess ? OQ_OK : cuda_fail(e, "fused append kernel");
-  }
-  // QJL keys: compress + append per role, through record scratch if needed
-  void* scratch = nullptr;
-  const size_t rbk = ck->p.rec_bytes, rbv = cv->p.rec_bytes;
-  if (!k_records || !v_records) {
-    cudaError_t e = cudaMallocAsync(&scratch, n_streams * (rbk + rbv), st);
-    if (e != cudaSuccess) return cuda_fail(e, "append scratch");
-  }
-  uint8_t* sk = static_cast<uint8_t*>(scratch);
-  s = oq_cache_append(ck, OQ_ROLE_K, k, dtype, n_streams, pos_dev, pos,
-                      k_records ? k_records : sk, ktiles, cap_tokens, stream);
-  if (!s)
-    s = oq_cache_append(cv, OQ_ROLE_V, v, dtype, n_streams, pos_dev, pos,
-                        v_records ? v_records : sk + n_streams * rbk, vtiles, cap_tokens, stream);
-  if (scratch) cudaFreeAsync(scratch, st);
-  return s;
+  // one launch: both roles encoded (exactly, QJL sidecar included) and
+  // written in place (the tile format implies d = 128)
+  cudaError_t e = oqd::launch_append_fused(
+      ck->p, cv->p, k, v, dtype, n_streams, pos_dev, pos, static_cast<uint8_t*>(k_records),
+      static_cast<uint8_t*>(v_records), static_cast<uint8_t*>(ktiles),
+      static_cast<uint8_t*>(vtiles), (cap_tokens + 31) / 32, st);
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "fused append kernel");
 }
 
 static int parts_per_row(const oq_codec* ck, const oq_attn_shape* sh, uint64_t t0, uint64_t t1,
