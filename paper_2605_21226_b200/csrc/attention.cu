@@ -1266,7 +1266,7 @@ __global__ void __launch_bounds__(32 * kAppendWarps) append_fused_kernel(
     uint8_t* __restrict__ rv, uint8_t* __restrict__ tk, uint8_t* __restrict__ tv,
     size_t tiles_cap) {
   __shared__ double row_s[kAppendWarps][132];
-  __shared__ uint32_t rec_s[kAppendWarps][32];
+  __shared__ uint32_t rec_s[kAppendWarps][kRecWords];
   __shared__ uint32_t run_s[kAppendWarps][32][21];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, role = blockIdx.y;
   const size_t s = blockIdx.x * (size_t)kAppendWarps + wib;

@@ -332,7 +332,7 @@ constexpr int kSmallWarps = 4;
 __global__ void __launch_bounds__(32 * kSmallWarps) compress_small_kernel(
     OqCodecParams p, const void* __restrict__ x, int dtype, size_t n, uint8_t* __restrict__ out) {
   __shared__ double row_s[kSmallWarps][132];
-  __shared__ uint32_t rec_s[kSmallWarps][32];
+  __shared__ uint32_t rec_s[kSmallWarps][kRecWords];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const size_t key = blockIdx.x * (size_t)kSmallWarps + wib;
   if (key >= n) return;
@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps) compress_rekey_kernel(
     OqCodecParams p, const void* __restrict__ x, int dtype, uint8_t* __restrict__ out,
     const FlagEntry* __restrict__ flags, const uint32_t* __restrict__ flag_cnt) {
   __shared__ double row_s[kSmallWarps][132];
-  __shared__ uint32_t rec_s[kSmallWarps][32];
+  __shared__ uint32_t rec_s[kSmallWarps][kRecWords];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t n = *flag_cnt;
   const uint32_t rb = p.rec_bytes;

@@ -10,6 +10,10 @@
 
 namespace oqd {
 
+// Record words a warp encoder stages: the largest d = 128 record (b_dir = 8,
+// b_nrm = 8, QJL) is 4 + 86 + 43 + 18 = 151 bytes.
+constexpr int kRecWords = 40;
+
 struct CompressSmem {
   double* xb;
   double* rb;
@@ -229,6 +233,7 @@ __device__ __forceinline__ void encode_key_warp(const OqCodecParams& p, const vo
     row[4 * lane + i] = dmul(k[i], k[i]);
   }
   rec[lane] = 0u;
+  if (lane < kRecWords - 32) rec[32 + lane] = 0u;
   __syncwarp();
   double g2 = 0.0;  // squares are rounded identically in parallel: only the adds chain
   if (lane == 0)
