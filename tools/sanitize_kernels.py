@@ -29,7 +29,11 @@ rv = torch.empty((B * Hkv, ev.record_bytes), dtype=torch.uint8, device=dev)
 cache.append(torch.randn((B, Hkv, 128), device=dev).to(torch.bfloat16),
              torch.randn((B, Hkv, 128), device=dev).to(torch.bfloat16),
              pos=torch.arange(B * Hkv, device=dev) + T, records=(rk, rv))
-# QJL keys: compress + insert per role
+# QJL keys: one-warp-per-key small batches, the certified pass + whole-key
+# rekey of its flagged keys (20000 keys), the fused append with QJL keys
+eq3 = oq.Encoder(oq.CodecConfig(b_dir=4, b_nrm=2, qjl=True, rotation_seed=9))
+eq3.compress(torch.randn((100, 128), device=dev, generator=g))
+eq3.compress(torch.randn((20000, 128), device=dev, generator=g))
 eq = oq.Encoder(oq.CodecConfig(b_dir=3, b_nrm=1, qjl=True, rotation_seed=7))
 ev2 = oq.Encoder(oq.CodecConfig(b_dir=3, b_nrm=1, rotation_seed=8))
 c2 = oq.KVCache(eq, ev2, B, Hkv, 64)
