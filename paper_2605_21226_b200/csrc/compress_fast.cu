@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kCFThreads, 1)
         n -= 32;
       }
     };
-#pragma unroll 1
+#pragma unroll 2  // two groups per iteration: more independent triplets in flight
     for (int q = 0; q < 11; ++q) {
       float e[12];
       {
