@@ -147,3 +147,26 @@ def test_rejects_bad_shapes(orc, cuda):
         oq.attention_decode(torch.from_numpy(d["q"][:, :7]).to(cuda), d["cache"])
     with pytest.raises(ValueError):  # more tokens than the cache holds
         oq.attention_decode(torch.from_numpy(d["q"]).to(cuda), d["cache"], T=41)
+
+
+def test_long_context_weighted_stream_k(orc, cuda):
+    """Contexts long enough for the weighted stream-K split (>= 512 tiles per
+    stream: every stream start counts as extra tile units) against the
+    reference, with ragged lengths and a partial token range."""
+    import torch
+    B, Hq, Hkv, T = 2, 14, 2, 20000
+    d = build(orc, cuda, B, Hq, Hkv, T, seed=9)
+    q = torch.from_numpy(d["q"]).to(cuda)
+    got = oq.attention_decode(q, d["cache"]).cpu().numpy()
+    assert rel_err(got, oracle_out(d, B, Hq, Hkv)).max() <= TOL
+    lens = [19999, 16400]
+    sl = torch.tensor(lens, dtype=torch.int32, device=cuda)
+    got = oq.attention_decode(q, d["cache"], seq_lens=sl).cpu().numpy()
+    assert rel_err(got, oracle_out(d, B, Hq, Hkv, lens=lens)).max() <= TOL
+    # two ranges of >= 512 tiles each, merged in order == one pass
+    parts = torch.stack([oq.attention_partials(q, d["cache"], 0, 3000),
+                         oq.attention_partials(q, d["cache"], 3000, T)])
+    rows = B * Hq
+    out = oq.attention_combine(d["cache"].enc_v, parts, rows, 2, 132, rows * 132)
+    full = oq.attention_decode(q, d["cache"]).cpu().numpy()
+    assert rel_err(out.reshape(B, Hq, 128).cpu().numpy(), full).max() <= TOL
