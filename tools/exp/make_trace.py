@@ -14,8 +14,10 @@ j = s.index("\n", i)
 s = s[:j + 1] + "  TR(0);\n" + s[j + 1:]
 k = s.index("  __syncthreads();\n\n  auto run = [&](const Seg& it, int nparts) {", i)
 s = s[:k] + "  __syncthreads();\n  TR(1);\n  int segc = 0;\n\n  auto run = [&](const Seg& it, int nparts) {" + s[k + len("  __syncthreads();\n\n  auto run = [&](const Seg& it, int nparts) {"):]
-s = s.replace("""    else load_qfrag(qf, P, it.sh, lane);
-    WarpState S;""", """    else load_qfrag(qf, P, it.sh, lane);
+s = s.replace("""      load_qfrag(qf, P, it.sh, lane);
+    }
+    WarpState S;""", """      load_qfrag(qf, P, it.sh, lane);
+    }
     TR(2 + 6 * segc);
     WarpState S;""", 1)
 s = s.replace("""    warp_state_out(S, merge + warp * 8 * kPartW, g, c);""", """    TR(3 + 6 * segc);
@@ -25,10 +27,10 @@ s = s.replace("""    merge_store<kAttnWarps>(P, it, merge, s_mf, tid, blockDim.x
     TR(5 + 6 * segc);""", 1)
 s = s.replace("""      __syncthreads();
       if (s_last) {
-        __threadfence();""", """      __syncthreads();
+        for (int w""", """      __syncthreads();
       TR(6 + 6 * segc);
       if (s_last) {
-        __threadfence();""", 1)
+        for (int w""", 1)
 s = s.replace("""    __syncthreads();
   };
 
