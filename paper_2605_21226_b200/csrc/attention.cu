@@ -660,10 +660,11 @@ __device__ __forceinline__ void merge_store(const AttnKParams& P, const Seg& it,
 // 8 hc + w of q (Encoder::prepare, codec.hpp:282-292) into smem, then every
 // lane gathers its mma B fragments (same layout as qprep_kernel).
 template <int QF>
-// pre: this warp's q row (head 8 hc + warp), already loaded, or null.
+// pre: this warp's q row (head 8 hc + warp), already loaded (use_pre).
 __device__ __forceinline__ void seg_qprep(uint32_t (&qf)[QF], const AttnKParams& P, int sh,
                                           float* qs, int warp, int nwarps, int lane,
-                                          const float4* pre = nullptr) {
+                                          bool use_pre = false,
+                                          float4 pre = make_float4(0.f, 0.f, 0.f, 0.f)) {
   const int hc = sh % P.HC, stream = sh / P.HC;
   const int b = stream / P.Hkv, kvh = stream % P.Hkv;
   const float log2e = 1.4426950408889634f;
@@ -673,7 +674,7 @@ __device__ __forceinline__ void seg_qprep(uint32_t (&qf)[QF], const AttnKParams&
     const int h = 8 * hc + w;
     if (h < P.G) {
       const float* q = P.q + ((size_t)b * P.Hq + (size_t)kvh * P.G + h) * 128;
-      const float4 q4 = pre && w == warp ? *pre : __ldg(reinterpret_cast<const float4*>(q) + lane);
+      const float4 q4 = use_pre && w == warp ? pre : __ldg(reinterpret_cast<const float4*>(q) + lane);
       float y[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -790,7 +791,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
   // table staging so its latency is hidden behind it
   int sh_pre = -1;
   float4 q_pre = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (P.fuse && P.streamk && kAttnWarps == 8) {
+  // (not with QJL: the extra live float4 makes that variant spill in its tile loop)
+  if (!QJL && P.fuse && P.streamk && kAttnWarps == 8) {
     const size_t V = P.tps + P.sko, U = (size_t)P.n_sh * V, G = gridDim.x;
     const size_t u0 = sk_bound(blockIdx.x, U, G), u1 = sk_bound(blockIdx.x + 1, U, G);
     for (size_t sh = u0 / V; sh * V < u1; ++sh)
@@ -828,7 +830,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
     if (tile < it.thi) load_tile<W, QJL>(ra, P, it.stream, tile, g, c, lane, lane);
     uint32_t qf[C::QF];
     if (P.fuse) {
-      seg_qprep(qf, P, it.sh, qs, warp, kAttnWarps, lane, it.sh == sh_pre ? &q_pre : nullptr);
+      seg_qprep(qf, P, it.sh, qs, warp, kAttnWarps, lane, it.sh == sh_pre, q_pre);
       sh_pre = -1;
     } else {
       load_qfrag(qf, P, it.sh, lane);
