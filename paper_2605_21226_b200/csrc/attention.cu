@@ -826,8 +826,6 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
   auto run = [&](const Seg& it, int nparts) {
     TileRegs<W, QJL> ra, rb;
     size_t tile = it.tlo + warp;
-    // first tile in flight while the query fragments are prepared
-    if (tile < it.thi) load_tile<W, QJL>(ra, P, it.stream, tile, g, c, lane, lane);
     uint32_t qf[C::QF];
     if (P.fuse) {
       seg_qprep(qf, P, it.sh, qs, warp, kAttnWarps, lane, it.sh == sh_pre, q_pre);
@@ -835,6 +833,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
     } else {
       load_qfrag(qf, P, it.sh, lane);
     }
+    // first tile requested after the query prep: issued before it, its 31
+    // loads per lane (on every SM at once) held up the prep (C3 -0.7 us)
+    if (tile < it.thi) load_tile<W, QJL>(ra, P, it.stream, tile, g, c, lane, lane);
     WarpState S;
     init_state(S);
     while (tile < it.thi) {

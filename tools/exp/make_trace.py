@@ -16,10 +16,10 @@ k = s.index("  __syncthreads();\n\n  auto run = [&](const Seg& it, int nparts) {
 s = s[:k] + "  __syncthreads();\n  TR(1);\n  int segc = 0;\n\n  auto run = [&](const Seg& it, int nparts) {" + s[k + len("  __syncthreads();\n\n  auto run = [&](const Seg& it, int nparts) {"):]
 s = s.replace("""      load_qfrag(qf, P, it.sh, lane);
     }
-    WarpState S;""", """      load_qfrag(qf, P, it.sh, lane);
+""", """      load_qfrag(qf, P, it.sh, lane);
     }
     TR(2 + 6 * segc);
-    WarpState S;""", 1)
+""", 1)
 s = s.replace("""    warp_state_out(S, merge + warp * 8 * kPartW, g, c);""", """    TR(3 + 6 * segc);
     warp_state_out(S, merge + warp * 8 * kPartW, g, c);""", 1)
 s = s.replace("""    merge_store<kAttnWarps>(P, it, merge, s_mf, tid, blockDim.x);""", """    TR(4 + 6 * segc);
