@@ -1440,7 +1440,9 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
       const char* e = getenv("OQ_ATTN_SKO");
       return e ? atol(e) : -1L;
     }();
-    P.sko = sko_env >= 0 ? (size_t)sko_env : (P.tps >= 512 ? 32 : 0);
+    // (swept with tools/exp/sko_sweep.sh: 48 best at 4096 tiles per stream,
+    // 32 at 1024)
+    P.sko = sko_env >= 0 ? (size_t)sko_env : (P.tps >= 2048 ? 48 : P.tps >= 512 ? 32 : 0);
   }
   int grid = P.n_items < num_sms ? P.n_items : num_sms;
   if (P.streamk) {
