@@ -438,13 +438,17 @@ __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL
   // The warp-wide max reduction (three dependent shuffles per head) runs only
   // when some lane's own scores exceed the running maximum; otherwise the max
   // cannot move, so the result is identical (C3/C5/C4 -3.5/-3.4/-2.2 %).
-  // Letting the max lag by up to 2^8 (rescale only on larger jumps) was a
-  // further -1.7 % on C5/C4 but +0.7 % on C3, and p * gamma_v would then need
-  // 8 bits of fp16 headroom, so it is not used.
+  // W = 10 (C3) keeps no lag: a lag of 2^8 was +0.7 % there (and needs 8
+  // bits of fp16 headroom in p * gamma_v); smaller lags were not measured on it.
   float lm[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) lm[h] = fmaxf(fmaxf(sc[0][h], sc[1][h]), fmaxf(sc[2][h], sc[3][h]));
-  if (__any_sync(kFull, lm[0] > S.m[0] || lm[1] > S.m[1])) {
+  // Byte-coded tiles (W <= 8) also let the max lag by up to 2 (log2 units):
+  // p <= 4 then, which costs 2 bits of fp16 headroom in p * gamma_v (overflow
+  // only past gamma_v ~ 16K) and skips the rescales of small max moves
+  // (C5 -1.2 %, C4 -0.7 %); (m, l, acc) stay consistent, so merges are exact.
+  constexpr float kLag = W <= 8 ? 2.f : 0.f;
+  if (__any_sync(kFull, lm[0] > S.m[0] + kLag || lm[1] > S.m[1] + kLag)) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       float v = lm[h];
