@@ -9,16 +9,19 @@ prints ONE JSON line on rank 0.
 Headline workload (BASELINE.json configs[2], "C3"): Qwen2.5-7B-shaped decode
 attention, B=8, 28 query / 4 KV heads, d=128, K=V 3-bit (b_dir 4, b_nrm 2),
 131072 cached tokens per rank.  A "step" = one decode-attention pass over the
-whole compressed cache (qprep + fused split-K attention + combine; with N>1
-ranks the cache is sequence-sharded: rank r holds its own 128K-token slice of
-an N*128K context and the partial (m, l, acc) states meet in ONE NCCL
-all-gather, then every rank merges them -> weak scaling).  The sharded step
-goes through the library's own oq_attention_decode_sharded (fused attention
-writes the rank's partial, ncclAllGather, merge); OQ_BENCH_NCCL=torch uses
-torch.distributed's all-gather instead, OQ_BENCH_SHARDED=1 runs it on one rank.
+whole compressed cache (query prep + fused split-K attention + merge in ONE
+launch).  With N>1 ranks the cache is sequence-sharded: rank r holds a
+contiguous slice of the context and the partial (m, l, acc) states meet in ONE
+NCCL all-gather, then every rank merges them (oq_attention_decode_sharded).
+  --config c3 / c4 (weak scaling): T tokens per rank, an N*T-token context;
+  --config c5 (strong scaling): the 1M-token context split over the N ranks.
+--gpus N launches N ranks itself (torch.distributed.run, 127.0.0.1) when
+WORLD_SIZE is unset; under an external launcher WORLD_SIZE must equal N.
+OQ_BENCH_NCCL=torch uses torch.distributed's all-gather instead of the
+library's NCCL call; OQ_BENCH_SHARDED=1 runs the sharded step on one rank.
 value = algorithmic compressed-KV bytes of all ranks (B*Hkv*T*(58+58) B per
-rank) / max-over-ranks step time.  Inputs (486 MB per rank) exceed the 126 MB
-L2, so no flush is needed between steps.
+rank at C3) / max-over-ranks step time.  Inputs (486 MB per rank at C3) exceed
+the 126 MB L2, so no flush is needed between steps.
 """
 from __future__ import annotations
 
@@ -39,14 +42,37 @@ BASELINE_METRIC = ("decode-attn compressed-KV GB/s (% HBM peak) & compress token
                    "1/2/4/8 B200")
 
 WORKLOADS = {
-    # name: (bits, qjl_on_K, B, Hq, Hkv, T_per_rank, description)
-    "c3": (3, False, 8, 28, 4, 131072, "C3: Qwen2.5-7B-shape decode attention, 3-bit K=V, "
-                                       "128K tokens/rank, B=8"),
-    "c4": (2, True, 32, 28, 4, 32768, "C4: OCTOPUS-QJL 2-bit K (+1-bit residual signs), "
-                                      "2-bit V, 32K tokens/rank, B=32"),
-    "c5": (2, False, 8, 28, 4, 131072, "C5: 2-bit K=V, 128K tokens/rank (1M-token context at "
-                                       "8 ranks), B=8"),
+    # name: (bits, qjl_on_K, B, Hq, Hkv, T, scaling, description).  Weak: T tokens
+    # per rank (N ranks hold an N*T-token context); strong: T tokens in total,
+    # sequence-sharded over the N ranks (T/N each).
+    "c3": (3, False, 8, 28, 4, 131072, "weak",
+           "C3: Qwen2.5-7B-shape decode attention, 3-bit K=V, 128K tokens/rank, B=8"),
+    "c4": (2, True, 32, 28, 4, 32768, "weak",
+           "C4: OCTOPUS-QJL 2-bit K (+1-bit residual signs), 2-bit V, 32K tokens/rank, B=32"),
+    "c5": (2, False, 8, 28, 4, 1 << 20, "strong",
+           "C5: 2-bit K=V, 1M-token context (2^20 tokens) sequence-sharded over the ranks, B=8"),
 }
+
+
+def tokens_per_rank(cfg, world):
+    bits, qjl, B, Hq, Hkv, T, scaling, desc = WORKLOADS[cfg]
+    if scaling == "weak":
+        return T
+    if T % world:
+        raise SystemExit(f"{cfg}: {T} tokens do not split over {world} ranks")
+    return T // world
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def rec_bytes(bits, qjl):
@@ -176,108 +202,148 @@ def build_cache(oq, torch, dev, bits, qjl, B, Hkv, T, seed, keep_host=0):
     return cache, host
 
 
+def time_attention(oq, torch, step, q, steps):
+    """(step_ms, kernel_ms) of `steps` calls of step(q): CUDA events around the
+    loop on the launching stream, plus the library's own per-launch events
+    around K3."""
+    for _ in range(3):
+        step(q)
+    torch.cuda.synchronize()
+    oq.timing(True)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        step(q)
+    e1.record(st)
+    torch.cuda.synchronize()
+    k_ms, k_n = oq.timing_collect("attention")
+    oq.timing(False)
+    return e0.elapsed_time(e1) / steps, k_ms / max(1, k_n)
+
+
+def kernel_name(bits, qjl):
+    return f"attn_partials_kernel<{3 * bits + 1}, {int(qjl)}, 8>"
+
+
 def other_configs(oq, torch, dev, peak, main_cfg, steps=20):
-    """K3 at the BASELINE configs other than the headline one (single GPU,
-    same method: device-resident cache, library CUDA events around K3)."""
+    """K3 at the BASELINE configs other than the headline one on this GPU (the
+    P = 1 point for C5), same method: device-resident cache, library CUDA
+    events around K3, traffic from the committed ncu capture."""
     res = {}
-    for name, (bits, qjl, B, Hq, Hkv, T, desc) in WORKLOADS.items():
+    for name, (bits, qjl, B, Hq, Hkv, T, scaling, desc) in WORKLOADS.items():
         if name == main_cfg:
             continue
         cache, _ = build_cache(oq, torch, dev, bits, qjl, B, Hkv, T, seed=7)
         q = torch.randn((B, Hq, 128), device=dev, generator=torch.Generator(device=dev).manual_seed(5))
         out = torch.empty((B, Hq, 128), dtype=torch.float32, device=dev)
-        for _ in range(3):
-            oq.attention_decode(q, cache, n_splits=0, out=out)
-        torch.cuda.synchronize()
-        oq.timing(True)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
-            oq.attention_decode(q, cache, n_splits=0, out=out)
-        e1.record()
-        torch.cuda.synchronize()
-        k_ms, k_n = oq.timing_collect("attention")
-        oq.timing(False)
-        kern = k_ms / max(1, k_n)
+        step_ms, kern = time_attention(
+            oq, torch, lambda qd: oq.attention_decode(qd, cache, n_splits=0, out=out), q, steps)
         nbytes = B * Hkv * T * (rec_bytes(bits, qjl) + rec_bytes(bits, False))
-        res[name] = {"workload": desc, "algorithmic_bytes": nbytes,
-                     "step_us": e0.elapsed_time(e1) / steps * 1e3, "kernel_us": kern * 1e3,
+        res[name] = {"workload": desc + (" (P = 1)" if scaling == "strong" else ""),
+                     "algorithmic_bytes": nbytes,
+                     "step_us": step_ms * 1e3, "kernel_us": kern * 1e3,
                      "kernel_gbs": nbytes / (kern * 1e-3) / 1e9,
-                     "frac": nbytes / (kern * 1e-3) / 1e9 / peak}
+                     "frac": nbytes / (kern * 1e-3) / 1e9 / peak,
+                     "kernel": kernel_name(bits, qjl),
+                     "traffic": ncu_traffic(kernel_name(bits, qjl))}
         del cache
         torch.cuda.empty_cache()
     return res
 
 
-def cpu_reference_sample(ref_lib, bits, qjl, seed, k_recs, v_recs, q, threads):
-    """One bounded sample of the workload on the reference CPU implementation:
-    Encoder::decode of the V records + attention_decode for every query head
-    of the sampled KV streams (fan-out over heads).  Returns (seconds, bytes)."""
+# ---------------------------------------------------------------------------
+def cpu_attention_caches(ref_lib, bits, qjl, seed, k_recs, v_recs):
+    """The sampled streams as reference CPU caches (CompressedKey vectors; the
+    records are unpacked once, outside the timed steps)."""
+    from oracle_bind import RefCache
     bd, bn = bits + 1, bits - 1
     ek = ref_lib.encoder(b_dir=bd, b_nrm=bn, rotation_seed=1000 + seed, qjl=qjl,
                          qjl_seed=2000 + seed)
     ev = ref_lib.encoder(b_dir=bd, b_nrm=bn, rotation_seed=3000 + seed)
-    n_streams = len(k_recs)
-    G = q.shape[1] // n_streams if q.ndim == 3 else q.shape[0] // n_streams
-    qh = q.reshape(n_streams, G, 128).astype(np.float64)
+    caches = [RefCache(ek, ev, k, v) for k, v in zip(k_recs, v_recs)]
+    nbytes = sum(k.shape[0] * (k.shape[1] + v.shape[1]) for k, v in zip(k_recs, v_recs))
+    return caches, nbytes
+
+
+def cpu_attention_sample(caches, q, threads):
+    """One step of the bounded sample on the reference CPU implementation:
+    per sampled stream, Encoder::decode of its V keys and attention_decode for
+    each query head of its GQA group (q: [n_streams, G, 128]).  Streams run
+    concurrently, each fanned out over G threads.  Returns seconds."""
+    import concurrent.futures as cf
+    G = q.shape[1]
+    qh = np.ascontiguousarray(q, np.float64)
+    inflight = max(1, threads // G)
     t0 = time.perf_counter()
-    res = [None] * n_streams
-
-    def work(s):
-        vals = ev.decode(v_recs[s], threads=max(1, threads // n_streams))
-        res[s] = ek.attention(qh[s], k_recs[s], vals, 1, threads=G)
-
-    ths = [threading.Thread(target=work, args=(s,)) for s in range(n_streams)]
-    for t in ths:
-        t.start()
-    for t in ths:
-        t.join()
+    with cf.ThreadPoolExecutor(inflight) as ex:
+        outs = list(ex.map(lambda s: caches[s].attention(qh[s], threads=G), range(len(caches))))
     dt = time.perf_counter() - t0
-    nbytes = sum(len(k) * (k.shape[1] + v_recs[i].shape[1]) for i, k in enumerate(k_recs))
-    return dt, nbytes
+    assert all(np.all(np.isfinite(o)) for o in outs)
+    return dt
+
+
+def cpu_encode_sample(ref_lib, bits, threads, n=1 << 18, seed=5):
+    """Reference Encoder::encode (local3x3, fp32 keys) of n Gaussian keys over
+    `threads` host threads: (keys/s, seconds)."""
+    bd, bn = bits + 1, bits - 1
+    enc = ref_lib.encoder(b_dir=bd, b_nrm=bn)
+    x = np.random.default_rng(seed).standard_normal((n, 128), np.float32)
+    enc.encode_f32(x[:4096], threads=threads)
+    t0 = time.perf_counter()
+    enc.encode_f32(x, threads=threads)
+    dt = time.perf_counter() - t0
+    return n / dt, dt
 
 
 # ---------------------------------------------------------------------------
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation (oracle/_ref,
-    compiled from /root/reference/proj/include) on this host's cores."""
+    compiled from /root/reference/proj/include) on this host's cores, on this
+    arm's config, metric and unit; rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle_bind import RefLib
-    bits, qjl, B, Hq, Hkv, T, desc = WORKLOADS[args.config]
+    world = args.gpus
+    bits, qjl, B, Hq, Hkv, T, scaling, desc = WORKLOADS[args.config]
+    Tr = tokens_per_rank(args.config, world)
     ref = RefLib()
     cores = os.cpu_count() or 1
-    Ts = min(T, 32768)
+    # bounded sample: whole batch entries (all KV streams and query heads of
+    # each) of one rank's token slice, at most ~0.5 GB of compressed KV
+    bpe = Hkv * Tr * (rec_bytes(bits, qjl) + rec_bytes(bits, False))
+    Bs = max(1, min(B, (512 << 20) // bpe))
     rng = np.random.default_rng(7)
     bd, bn = bits + 1, bits - 1
     seed = 0
     ek = ref.encoder(b_dir=bd, b_nrm=bn, rotation_seed=1000 + seed, qjl=qjl, qjl_seed=2000 + seed)
     ev = ref.encoder(b_dir=bd, b_nrm=bn, rotation_seed=3000 + seed)
-    k_recs = [ek.encode_f32(rng.standard_normal((Ts, 128), np.float32), threads=cores)
-              for _ in range(Hkv)]
-    v_recs = [ev.encode_f32(rng.standard_normal((Ts, 128), np.float32), threads=cores)
-              for _ in range(Hkv)]
-    q = rng.standard_normal((Hq, 128)).astype(np.float32)
-    for _ in range(max(1, args.warmup)):
-        cpu_reference_sample(ref, bits, qjl, seed, k_recs, v_recs, q, cores)
-    ts, nb = [], 0
-    for _ in range(args.steps):
-        dt, nb = cpu_reference_sample(ref, bits, qjl, seed, k_recs, v_recs, q, cores)
-        ts.append(dt)
+    k_recs, v_recs = [], []
+    for _ in range(Bs * Hkv):
+        k_recs.append(ek.encode_f32(rng.standard_normal((Tr, 128), np.float32), threads=cores))
+        v_recs.append(ev.encode_f32(rng.standard_normal((Tr, 128), np.float32), threads=cores))
+    q = rng.standard_normal((Bs * Hkv, Hq // Hkv, 128)).astype(np.float32)
+    caches, nb = cpu_attention_caches(ref, bits, qjl, seed, k_recs, v_recs)
+    del k_recs, v_recs
+    for _ in range(max(1, min(args.warmup, 2))):
+        cpu_attention_sample(caches, q, cores)
+    ts = [cpu_attention_sample(caches, q, cores) for _ in range(args.steps)]
     tot = sum(ts)
     gbs = nb * len(ts) / tot / 1e9
-    sample = (f"1 batch entry x {Hkv} KV streams x {Ts} tokens x {Hq} query heads "
-              f"(Encoder::decode of V + attention_decode per head)")
+    full = B * Hkv * Tr * world * (rec_bytes(bits, qjl) + rec_bytes(bits, False))
+    sample = (f"{Bs} of {B} batch entries x {Hkv} KV streams x {Tr} tokens x {Hq} query heads "
+              f"({nb / full:.3g} of the {world}-rank step's compressed bytes): Encoder::decode "
+              f"of V + attention_decode per (stream, head) on {cores} threads")
     line = {
         "impl": "reference", "metric": BASELINE_METRIC, "value": gbs, "unit": "GB/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot / len(ts), "higher_is_better": True, "scaling": "weak",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(ts), "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic Gaussian (numpy)",
-        "config": workload_config(args, 1, None),
-        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "reference",
-                         "sample": sample},
+        "config": workload_config(args, world, 0),
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "cpu_model": cpu_model(),
+                         "kind": "reference", "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -285,14 +351,29 @@ def run_reference(args):
 
 
 def workload_config(args, world, splits):
-    bits, qjl, B, Hq, Hkv, T, desc = WORKLOADS[args.config]
+    bits, qjl, B, Hq, Hkv, T, scaling, desc = WORKLOADS[args.config]
+    Tr = tokens_per_rank(args.config, world)
     return {"workload": desc, "B": B, "Hq": Hq, "Hkv": Hkv, "d": 128, "bits": bits,
             "b_dir": bits + 1, "b_nrm": bits - 1, "rounding": "local3x3", "qjl_on_K": qjl,
-            "tokens_per_rank": T, "context_tokens": T * world,
+            "tokens_per_rank": Tr, "context_tokens": Tr * world,
             "record_bytes_K": rec_bytes(bits, qjl), "record_bytes_V": rec_bytes(bits, False),
             "splits": splits, "parallelism": f"sequence-sharded x{world} (NCCL all-gather of "
                                              "softmax partials)" if world > 1 else "single GPU",
             "l2": "no flush: per-rank inputs > 126 MB L2"}
+
+
+def spawn_ranks(args):
+    """--gpus N without an external launcher: run this script under
+    torch.distributed.run with N ranks on 127.0.0.1 and return its exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -308,8 +389,15 @@ def main():
                     help="skip the K3 timings at the non-headline BASELINE configs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None and int(env_world) != args.gpus:
+        raise SystemExit(f"WORLD_SIZE={env_world} disagrees with --gpus {args.gpus}")
     if args.impl == "reference":
         return run_reference(args)
+    if env_world is None and args.gpus > 1:
+        return spawn_ranks(args)
 
     import torch
     import torch.distributed as dist
@@ -331,7 +419,8 @@ def main():
             os.environ.setdefault("RANK", "0")
         dist.init_process_group("nccl", device_id=dev, world_size=world, rank=rank)
 
-    bits, qjl, B, Hq, Hkv, T, desc = WORKLOADS[args.config]
+    bits, qjl, B, Hq, Hkv, T_cfg, scaling, desc = WORKLOADS[args.config]
+    T = tokens_per_rank(args.config, world)
     keep = Hkv if (rank == 0 and world == 1 and not args.no_cpu_baseline) else 0
     cache, host = build_cache(oq, torch, dev, bits, qjl, B, Hkv, T, seed=rank, keep_host=keep)
     rows = B * Hq
@@ -347,20 +436,31 @@ def main():
     # C call) or through torch.distributed (OQ_BENCH_NCCL=torch)
     native = sharded and os.environ.get("OQ_BENCH_NCCL", "native") == "native"
     comm = None
+    nccl_info = None
     if native:
         uid = [oq.NcclComm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = oq.NcclComm(world, uid[0], rank)
+        r_nccl, n_nccl = comm.info()
+        if n_nccl != world or r_nccl != rank:
+            raise SystemExit(f"NCCL communicator reports rank {r_nccl} of {n_nccl}, expected "
+                             f"{rank} of {world}")
+        nccl_info = {"rank": r_nccl, "nranks": n_nccl, "source": "ncclCommUserRank/ncclCommCount"}
 
-    def step(qd):
-        if not sharded:
-            return oq.attention_decode(qd, cache, n_splits=splits, out=out)
-        if native:
-            return oq.attention_decode_sharded(qd, cache, 0, T, comm, n_splits=splits, out=out)
-        part = oq.attention_partials(qd, cache, 0, T, n_splits=splits)
-        dist.all_gather_into_tensor(gathered, part)
-        return oq.attention_combine(cache.enc_v, gathered, rows, world, 132, rows * 132,
-                                    out=out.view(rows, 128))
+    def make_step(cache_, out_, gathered_, rows_):
+        def step(qd):
+            if not sharded:
+                return oq.attention_decode(qd, cache_, n_splits=splits, out=out_)
+            if native:
+                return oq.attention_decode_sharded(qd, cache_, 0, cache_.tokens, comm,
+                                                   n_splits=splits, out=out_)
+            part = oq.attention_partials(qd, cache_, 0, cache_.tokens, n_splits=splits)
+            dist.all_gather_into_tensor(gathered_, part)
+            return oq.attention_combine(cache_.enc_v, gathered_, rows_, world, 132, rows_ * 132,
+                                        out=out_.view(rows_, 128))
+        return step
+
+    step = make_step(cache, out, gathered, rows)
 
     def barrier():
         if world > 1:
@@ -419,6 +519,35 @@ def main():
     clk.__exit__(None, None, None)
     e2e_val = world * alg_bytes_rank * args.steps / (e2e_ms * 1e-3) / 1e9
 
+    # ---- C5: the latency-bound B = 1 case of the same sharded context -----------
+    b1 = None
+    if args.config == "c5":
+        cache1, _ = build_cache(oq, torch, dev, bits, qjl, 1, Hkv, T, seed=100 + rank)
+        out1 = torch.empty((1, Hq, 128), dtype=torch.float32, device=dev)
+        g1 = torch.empty((world * Hq, 132), dtype=torch.float32, device=dev)
+        step1 = make_step(cache1, out1, g1, Hq)
+        q1 = q[:1].contiguous()
+        for _ in range(args.warmup):
+            step1(q1)
+        torch.cuda.synchronize()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            step1(q1)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        t = torch.tensor([f0.elapsed_time(f1)], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms1 = float(t.item()) / args.steps
+        by1 = world * Hkv * T * (rec_bytes(bits, qjl) + rec_bytes(bits, False))
+        b1 = {"what": "B = 1 (latency-bound): one sequence of the same context, same path",
+              "value": by1 / (ms1 * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms1}
+        del cache1
+        torch.cuda.empty_cache()
+
     # ---- one decoder step: append the new token's K and V of every stream ------
     # (compress + write into its tile slot), then attention over T+1 tokens
     step_info = None
@@ -443,7 +572,7 @@ def main():
         st = a1.elapsed_time(a2) / args.steps
         step_info = {"what": "decoder step: bf16 K/V of B*Hkv streams appended (one fused exact "
                              "encode + tile insert launch for K and V) then decode attention over "
-                             "the 128K-token cache",
+                             "the cache",
                      "append_us": ap * 1e3, "append_plus_attention_us": st * 1e3}
         # the same step captured once in a CUDA graph and replayed (how a serving
         # loop removes the per-launch host overhead of the small append kernels)
@@ -478,9 +607,11 @@ def main():
     if not args.no_compress:
         comp = bench_compress(oq, torch, dev, bits, world, barrier, dist, peak)
 
-    # ---- K3 at the other BASELINE configs (C4 QJL, C5 2-bit) ---------------------
+    # ---- K3 at the other BASELINE configs (C4 QJL, C5 2-bit at P = 1) -----------
     others = None
     if world == 1 and not args.no_other_configs:
+        del cache
+        torch.cuda.empty_cache()
         others = other_configs(oq, torch, dev, peak, args.config)
 
     # ---- CPU baseline: the reference implementation on this host ----------------
@@ -493,30 +624,38 @@ def main():
         Ts = min(T, 32768)
         kr = [h[:Ts] for h in host["k"]]
         vr = [h[:Ts] for h in host["v"]]
-        qs = q_host[0].numpy()
-        dts, nb = [], 0
+        qs = q_host[0].numpy().reshape(Hkv, Hq // Hkv, 128)
+        caches, nb = cpu_attention_caches(ref, bits, qjl, rank, kr, vr)
+        cpu_attention_sample(caches, qs, cores)
+        dts = []
         t_end = time.perf_counter() + 8.0
         while time.perf_counter() < t_end or not dts:
-            dt, nb = cpu_reference_sample(ref, bits, qjl, rank, kr, vr, qs, cores)
-            dts.append(dt)
+            dts.append(cpu_attention_sample(caches, qs, cores))
         cpu = {"value": nb * len(dts) / sum(dts) / 1e9, "unit": "GB/s", "cores": cores,
-               "kind": "reference",
+               "cpu_model": cpu_model(), "kind": "reference",
                "sample": f"batch entry 0: {Hkv} KV streams x {Ts} tokens x {Hq} query heads, "
-                         f"V decoded by Encoder::decode + attention_decode per head; "
+                         f"V decoded by Encoder::decode + attention_decode per (stream, head); "
                          f"{len(dts)} repeats, {sum(dts):.1f} s"}
+        if comp is not None:
+            kps, dt = cpu_encode_sample(ref, bits, cores)
+            comp["cpu_baseline"] = {
+                "value": kps, "unit": "tokens/s", "cores": cores, "cpu_model": cpu_model(),
+                "kind": "reference",
+                "sample": f"Encoder::encode of 2^18 fp32 Gaussian keys (local3x3, b={bits}) on "
+                          f"{cores} threads, {dt:.2f} s"}
 
     if rank == 0:
         line = {
             "metric": BASELINE_METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "u8 codes -> f16 mma, f32 accumulate",
             "data": "synthetic (torch.randn K/V/Q, K/V compressed on device by K1)",
             "config": workload_config(args, world, splits),
             "hbm_frac_of_peak": value / world / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
-                         "traffic": ncu_traffic(f"attn_partials_kernel<{3 * bits + 1}, {int(qjl)}, 8>"),
+                         "traffic": ncu_traffic(kernel_name(bits, qjl)),
                          "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/)",
                          "kernel": "attn_partials_kernel (K3)",
                          "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": alg_bytes_rank},
@@ -529,6 +668,8 @@ def main():
             # world 1: one fused K3 launch per step; sharded: the fused K3
             # (writing this rank's partial) + the merge after the NCCL all-gather
             "gpu_launches": (2 if sharded else 1) * args.steps,
+            "nccl": nccl_info,
+            "b1": b1,
             "compress": comp,
             "decode_step": step_info,
             "other_configs": others,

@@ -100,6 +100,46 @@ oq_status oq_compress_ex(const oq_codec* codec, const void* x, int dtype, size_t
 oq_status oq_decode(const oq_codec* codec, const void* records, size_t n, float* out,
                     void* stream);
 
+/* ---- the per-key Encoder API in exact fp64 ------------------------------
+ * Bit-identical to the reference (fp64, its evaluation order, no FMA
+ * contraction); these back the drop-in C++ header's per-key methods.
+ * Direction table (host, no device needed): out fp64 [k*k][3] =
+ * oct_decode(xi_a, xi_b) for the k xi centroids — the reference's
+ * build_dir_table / Books::dirs (codec.hpp:96-141). */
+oq_status oq_dir_table(const double* xi_centroids, int k, double* out);
+/* Encoder::prepare (codec.hpp:282-292): q device fp64 [nq, dim] -> rot = R q
+ * and, for a QJL codec, sketch = R' R q (device fp64 [nq, dim]; sketch may be
+ * NULL without QJL). */
+oq_status oq_prepare_f64(const oq_codec* codec, const double* q, size_t nq, double* rot,
+                         double* sketch, void* stream);
+/* Encoder::reconstruct_rotated (codec.hpp:252-266): records -> device fp64
+ * [n, dim], unit scale, rotated frame. */
+oq_status oq_reconstruct_rotated(const oq_codec* codec, const void* records, size_t n,
+                                 double* out, void* stream);
+/* Encoder::decode (codec.hpp:268-275) in exact fp64: records -> device fp64
+ * [n, dim].  (oq_decode is the fp32 throughput path, rel. err <= 1e-5.) */
+oq_status oq_decode_f64(const oq_codec* codec, const void* records, size_t n, double* out,
+                        void* stream);
+/* Encoder::score(prepared, k) + qjl_estimate (codec.hpp:295-311,
+ * qjl.hpp:39-48): prepared rot/sketch device fp64 [nq, dim] x n records ->
+ * out device fp64 [nq][n]. */
+oq_status oq_score_prepared(const oq_codec* codec, const double* rot, const double* sketch,
+                            size_t nq, const void* records, size_t n, double* out,
+                            void* stream);
+
+/* attention_decode(enc, q, keys, values, n_splits) (attention.hpp:50-73) in
+ * fp64: Encoder::prepare + Encoder::score bit-exact, then the SoftmaxState
+ * push/merge recurrence per value column on the device (device exp: agrees
+ * with the reference to a few ulp).  q device fp64 [nq, dim], values device
+ * fp64 [n, vdim] -> out device fp64 [nq, vdim].  The drop-in C++ header's
+ * attention_decode; the throughput paths are oq_attention_decode (compressed
+ * V) and oq_attention_decode_dense (fp32). */
+size_t oq_attention_f64_workspace_bytes(const oq_codec* codec, size_t nq, size_t n);
+oq_status oq_attention_decode_f64(const oq_codec* codec, const double* q, size_t nq,
+                                  const void* records, size_t n, const double* values, int vdim,
+                                  int n_splits, double* out, void* workspace, size_t ws_bytes,
+                                  void* stream);
+
 /* ---- wire: pack_keys / unpack_keys (codec.hpp:364-478) -------------------
  * An OCTO v1 blob is oq_wire_header(...) followed by the records. */
 oq_status oq_wire_header(const oq_config* cfg, uint64_t count, uint8_t header[20]);
@@ -201,6 +241,8 @@ oq_status oq_attention_decode_sharded(const oq_codec* ck, const oq_codec* cv,
 oq_status oq_nccl_get_unique_id(uint8_t id[128]);
 oq_status oq_nccl_comm_init_rank(void** comm, int nranks, const uint8_t id[128], int rank);
 oq_status oq_nccl_comm_destroy(void* comm);
+/* ncclCommUserRank / ncclCommCount of a communicator (bench.py prints them). */
+oq_status oq_nccl_comm_info(void* comm, int* rank, int* nranks);
 
 /* ---- general path: any codec configuration, straight from OCTO records ----
  * Encoder::score(prepare(q), k) (codec.hpp:282-316): out[nq][n] fp32 for q

@@ -187,4 +187,65 @@ size_t ref_unpack_repack(const uint8_t* blob, size_t n, uint8_t* out) {
   }
 }
 
+
+
+// ---- CPU-resident compressed cache (bench.py's reference arm) --------------
+// A reference user holds the cache as CompressedKey vectors; the records are
+// unpacked once here (not per step).  Each step then runs what the reference
+// needs for decode attention over a compressed K AND V cache:
+// Encoder::decode of every V key into the values Matrix, and
+// attention_decode(enc_k, q, keys, values) per query of the GQA group.
+struct RefCache {
+  const Encoder* ek;
+  const Encoder* ev;
+  std::vector<CompressedKey> keys, vals;
+};
+
+void* ref_cache_new(void* hk, void* hv, const uint8_t* krecs, const uint8_t* vrecs, size_t n) {
+  try {
+    auto* c = new RefCache{static_cast<Encoder*>(hk), static_cast<Encoder*>(hv), {}, {}};
+    c->keys = unpack_records(c->ek->config(), krecs, n);
+    c->vals = unpack_records(c->ev->config(), vrecs, n);
+    return c;
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+void ref_cache_free(void* h) { delete static_cast<RefCache*>(h); }
+
+int ref_cache_attention(void* h, const double* q, size_t nq, double* out, int threads) {
+  const RefCache& c = *static_cast<RefCache*>(h);
+  const uint32_t d = c.ek->config().dim, vd = c.ev->config().dim;
+  const size_t n = c.keys.size();
+  int bad = 0;
+  try {
+    Matrix vals(n, vd);
+    fan_out(n, threads, [&](size_t lo, size_t hi) {
+      try {
+        for (size_t i = lo; i < hi; ++i) {
+          const auto u = c.ev->decode(c.vals[i]);
+          std::memcpy(vals.row(i), u.data(), vd * 8);
+        }
+      } catch (...) {
+        bad = 1;
+      }
+    });
+    fan_out(nq, threads, [&](size_t lo, size_t hi) {
+      try {
+        for (size_t i = lo; i < hi; ++i) {
+          const auto o = attention_decode(*c.ek, std::span<const double>(q + i * d, d), c.keys,
+                                          vals, 1);
+          std::memcpy(out + i * vd, o.data(), vd * 8);
+        }
+      } catch (...) {
+        bad = 1;
+      }
+    });
+  } catch (...) {
+    return -1;
+  }
+  return bad ? -1 : 0;
+}
+
 }  // extern "C"

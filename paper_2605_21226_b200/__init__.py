@@ -100,6 +100,7 @@ def lib():
         "oq_nccl_get_unique_id": ([vp], i32),
         "oq_nccl_comm_init_rank": ([C.POINTER(vp), i32, vp, i32], i32),
         "oq_nccl_comm_destroy": ([vp], i32),
+        "oq_nccl_comm_info": ([vp, C.POINTER(i32), C.POINTER(i32)], i32),
         "oq_cache_append": ([vp, i32, vp, i32, C.c_uint64, vp, C.c_int64, vp, vp, C.c_uint64, vp],
                             i32),
         "oq_cache_append_kv": ([vp, vp, vp, vp, i32, C.c_uint64, vp, C.c_int64, vp, vp, vp, vp,
@@ -120,6 +121,13 @@ def lib():
         "oq_scores": ([vp, vp, i32, vp, sz, vp, vp], i32),
         "oq_attention_dense_workspace_bytes": ([i32, i32, i32], sz),
         "oq_attention_decode_dense": ([vp, vp, i32, vp, sz, vp, i32, i32, vp, vp, sz, vp], i32),
+        "oq_dir_table": ([dp, i32, dp], i32),
+        "oq_prepare_f64": ([vp, vp, sz, vp, vp, vp], i32),
+        "oq_reconstruct_rotated": ([vp, vp, sz, vp, vp], i32),
+        "oq_decode_f64": ([vp, vp, sz, vp, vp], i32),
+        "oq_score_prepared": ([vp, vp, vp, sz, vp, sz, vp, vp], i32),
+        "oq_attention_f64_workspace_bytes": ([vp, sz, sz], sz),
+        "oq_attention_decode_f64": ([vp, vp, sz, vp, sz, vp, i32, i32, vp, vp, sz, vp], i32),
         "oq_timing_enable": ([i32], None),
         "oq_timing_collect": ([C.c_char_p, C.POINTER(C.c_double), C.POINTER(i32)], i32),
     }
@@ -338,6 +346,68 @@ class Encoder:
     def tile_bytes(self, role):
         return lib().oq_cache_tile_bytes(self._h, role)
 
+    # -- the per-key reference API in exact fp64 (bit-identical) --------------
+    def prepare(self, q, stream=None):
+        """Encoder::prepare (codec.hpp:282-292) for q [nq, dim]: (rot, sketch)
+        float64 CUDA tensors (sketch None without QJL), bit-identical."""
+        import torch
+        q = q.contiguous().to(torch.float64).reshape(-1, self.cfg.dim)
+        rot = torch.empty_like(q)
+        sk = torch.empty_like(q) if self.cfg.qjl else None
+        _check(lib().oq_prepare_f64(self._h, _ptr(q), q.shape[0], _ptr(rot),
+                                    None if sk is None else _ptr(sk), _stream(stream)))
+        return rot, sk
+
+    def reconstruct_rotated(self, records, stream=None):
+        """Encoder::reconstruct_rotated (codec.hpp:252-266): float64 [n, dim]."""
+        import torch
+        records = records.contiguous()
+        n = records.numel() // self.record_bytes
+        out = torch.empty((n, self.cfg.dim), dtype=torch.float64, device=records.device)
+        _check(lib().oq_reconstruct_rotated(self._h, _ptr(records), n, _ptr(out),
+                                            _stream(stream)))
+        return out
+
+    def decode_exact(self, records, stream=None):
+        """Encoder::decode (codec.hpp:268-275) in exact fp64: float64 [n, dim]."""
+        import torch
+        records = records.contiguous()
+        n = records.numel() // self.record_bytes
+        out = torch.empty((n, self.cfg.dim), dtype=torch.float64, device=records.device)
+        _check(lib().oq_decode_f64(self._h, _ptr(records), n, _ptr(out), _stream(stream)))
+        return out
+
+    def score_prepared(self, rot, sketch, records, stream=None):
+        """Encoder::score(prepared, k) (codec.hpp:295-311): float64 [nq, n]."""
+        import torch
+        records = records.contiguous()
+        n = records.numel() // self.record_bytes
+        rot = rot.contiguous().to(torch.float64)
+        out = torch.empty((rot.shape[0], n), dtype=torch.float64, device=records.device)
+        sk = None if sketch is None else _ptr(sketch.contiguous().to(torch.float64))
+        _check(lib().oq_score_prepared(self._h, _ptr(rot), sk, rot.shape[0], _ptr(records), n,
+                                       _ptr(out), _stream(stream)))
+        return out
+
+    def attention_exact(self, q, records, values, n_splits=1, stream=None):
+        """attention_decode(enc, q, keys, values, n_splits) in fp64 on the GPU
+        (attention.hpp:50-73): q [nq, dim], values [n, vdim] -> [nq, vdim]."""
+        import torch
+        q = q.contiguous().to(torch.float64).reshape(-1, self.cfg.dim)
+        values = values.contiguous().to(torch.float64)
+        records = records.contiguous()
+        n = records.numel() // self.record_bytes
+        if values.shape[0] != n:
+            raise ValueError("values/cache length mismatch")
+        L = lib()
+        wsb = L.oq_attention_f64_workspace_bytes(self._h, q.shape[0], n)
+        ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=q.device)
+        out = torch.empty((q.shape[0], values.shape[1]), dtype=torch.float64, device=q.device)
+        _check(L.oq_attention_decode_f64(self._h, _ptr(q), q.shape[0], _ptr(records), n,
+                                         _ptr(values), values.shape[1], n_splits, _ptr(out),
+                                         _ptr(ws), ws.numel(), _stream(stream)))
+        return out
+
 
 def pack_keys(cfg: CodecConfig, records):
     """pack_keys (codec.hpp:364-396): 20-byte OCTO header + records."""
@@ -466,22 +536,56 @@ def default_splits(B, Hkv, Hq, T, num_sms=None):
 
 
 class _Workspace:
+    """Per-(device, stream, kind) device scratch for the attention calls.
+
+    The tile-attention workspace's first 64 KiB are arrival counters the fused
+    kernel requires to be zero on entry (and leaves at zero), so one buffer is
+    never shared between streams: calls on different streams would race on the
+    counters and partials.  A buffer is allocated and zero-filled ON the launch
+    stream (ordered before the kernel that first uses it).  A buffer that is
+    outgrown is retired, never freed: a kernel still in flight or a captured
+    CUDA graph may reference it."""
     buf = {}
+    _retired = []
 
     @classmethod
-    def get(cls, nbytes, device, kind="tile"):
-        """kind "tile": the compressed-cache attention workspace (its first
-        64 KiB are arrival counters that must stay zero between calls, so it is
-        never shared with other scratch uses); "dense": the general path."""
+    def get(cls, nbytes, device, stream, kind="tile"):
         import torch
-        key = (str(device), kind)
+        key = (str(device), int(stream.cuda_stream), kind)
         b = cls.buf.get(key)
         if b is None or b.numel() < nbytes:
-            # zeroed once: the attention kernels keep their arrival counters
-            # (the first 64 KiB) at zero between calls
-            b = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            if b is not None:
+                cls._retired.append(b)
+            with torch.cuda.stream(stream):
+                b = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
             cls.buf[key] = b
         return b
+
+
+def _launch_stream(stream, device):
+    """The torch stream a call launches on (the caller's, or the current one)."""
+    import torch
+    return stream if stream is not None else torch.cuda.current_stream(device)
+
+
+def _check_query(q, cache):
+    if not q.is_cuda:
+        raise ValueError("q must be a CUDA tensor (there is no CPU path)")
+    if q.dim() != 3 or q.shape[0] != cache.B:
+        raise ValueError("q must be [B, Hq, dim] with B matching the cache")
+    if q.shape[-1] != cache.enc_k.cfg.dim:
+        raise ValueError("query dimension mismatch")
+
+
+def _check_seq_lens(seq_lens, B, device):
+    import torch
+    if seq_lens is None:
+        return
+    if (not seq_lens.is_cuda or seq_lens.dtype != torch.int32 or seq_lens.dim() != 1
+            or seq_lens.numel() != B or seq_lens.device != device):
+        raise ValueError("seq_lens must be an int32 CUDA tensor of length B on q's device")
+    if not seq_lens.is_contiguous():
+        raise ValueError("seq_lens must be contiguous")
 
 
 def _shape(cache: KVCache, Hq, T, seq_lens):
@@ -495,9 +599,13 @@ def attention_decode(q, cache: KVCache, n_splits=None, seq_lens=None, T=None, ou
 
     q: CUDA float32 [B, Hq, dim].  Returns [B, Hq, dim] float32.  n_splits:
     None/0 = stream-K (balanced over the SMs); k >= 1 = k contiguous chunks
-    per stream, the reference's n_splits.
+    per stream, the reference's n_splits.  seq_lens: optional int32 CUDA [B].
+    Everything (scratch, the fp32 copy of q, out) is allocated on the launch
+    stream, ``stream`` or the current one.
     """
     import torch
+    _check_query(q, cache)
+    _check_seq_lens(seq_lens, cache.B, q.device)
     B, Hq, D = q.shape
     T = cache.tokens if T is None else T
     if n_splits is None:
@@ -506,13 +614,15 @@ def attention_decode(q, cache: KVCache, n_splits=None, seq_lens=None, T=None, ou
     L = lib()
     ws_bytes = L.oq_attention_workspace_bytes(cache.enc_k.handle, cache.enc_v.handle,
                                               C.byref(sh), n_splits)
-    ws = _Workspace.get(ws_bytes, q.device)
-    if out is None:
-        out = torch.empty((B, Hq, D), dtype=torch.float32, device=q.device)
-    q = q.contiguous().float()
-    _check(L.oq_attention_decode(cache.enc_k.handle, cache.enc_v.handle, C.byref(sh), _ptr(q),
-                                 _ptr(cache.k), _ptr(cache.v), _ptr(out), n_splits, _ptr(ws),
-                                 ws.numel(), _stream(stream)))
+    st = _launch_stream(stream, q.device)
+    with torch.cuda.stream(st):
+        ws = _Workspace.get(ws_bytes, q.device, st)
+        if out is None:
+            out = torch.empty((B, Hq, D), dtype=torch.float32, device=q.device)
+        q = q.contiguous().float()
+        _check(L.oq_attention_decode(cache.enc_k.handle, cache.enc_v.handle, C.byref(sh),
+                                     _ptr(q), _ptr(cache.k), _ptr(cache.v), _ptr(out), n_splits,
+                                     _ptr(ws), ws.numel(), C.c_void_p(st.cuda_stream)))
     return out
 
 
@@ -521,20 +631,24 @@ def attention_decode_dense(enc: Encoder, q, records, values, n_splits=1, stream=
     codec config: q [nq, dim] fp32, keys as OCTO records [n], dense values
     [n, vdim] fp32 -> [nq, vdim]."""
     import torch
-    q = q.contiguous().float().reshape(-1, enc.cfg.dim)
-    records = records.contiguous()
-    values = values.contiguous().float()
-    n = records.numel() // enc.record_bytes
-    nq, vdim = q.shape[0], values.shape[-1] if values.dim() > 1 else 1
-    if values.shape[0] != n:
-        raise ValueError("values/cache length mismatch")
-    L = lib()
-    ws_bytes = L.oq_attention_dense_workspace_bytes(nq, max(1, n_splits), vdim)
-    ws = _Workspace.get(ws_bytes, q.device, kind="dense")
-    out = torch.empty((nq, vdim), dtype=torch.float32, device=q.device)
-    _check(L.oq_attention_decode_dense(enc.handle, _ptr(q), nq, _ptr(records), n, _ptr(values),
-                                       vdim, n_splits, _ptr(out), _ptr(ws), ws.numel(),
-                                       _stream(stream)))
+    if q.shape[-1] != enc.cfg.dim:
+        raise ValueError("query dimension mismatch")
+    st = _launch_stream(stream, q.device)
+    with torch.cuda.stream(st):
+        q = q.contiguous().float().reshape(-1, enc.cfg.dim)
+        records = records.contiguous()
+        values = values.contiguous().float()
+        n = records.numel() // enc.record_bytes
+        nq, vdim = q.shape[0], values.shape[-1] if values.dim() > 1 else 1
+        if values.shape[0] != n:
+            raise ValueError("values/cache length mismatch")
+        L = lib()
+        ws_bytes = L.oq_attention_dense_workspace_bytes(nq, max(1, n_splits), vdim)
+        ws = _Workspace.get(ws_bytes, q.device, st, kind="dense")
+        out = torch.empty((nq, vdim), dtype=torch.float32, device=q.device)
+        _check(L.oq_attention_decode_dense(enc.handle, _ptr(q), nq, _ptr(records), n,
+                                           _ptr(values), vdim, n_splits, _ptr(out), _ptr(ws),
+                                           ws.numel(), C.c_void_p(st.cuda_stream)))
     return out
 
 
@@ -542,6 +656,8 @@ def attention_partials(q, cache: KVCache, t_begin, t_end, n_splits=None, T=None,
                        out=None, stream=None):
     """SoftmaxState of tokens [t_begin, t_end) per (b, q head): [B*Hq, 132] fp32."""
     import torch
+    _check_query(q, cache)
+    _check_seq_lens(seq_lens, cache.B, q.device)
     B, Hq, D = q.shape
     T = cache.tokens if T is None else T
     if n_splits is None:
@@ -550,13 +666,16 @@ def attention_partials(q, cache: KVCache, t_begin, t_end, n_splits=None, T=None,
     L = lib()
     ws_bytes = L.oq_attention_workspace_bytes(cache.enc_k.handle, cache.enc_v.handle,
                                               C.byref(sh), n_splits)
-    ws = _Workspace.get(ws_bytes, q.device)
-    if out is None:
-        out = torch.empty((B * Hq, 4 + D), dtype=torch.float32, device=q.device)
-    q = q.contiguous().float()
-    _check(L.oq_attention_partials(cache.enc_k.handle, cache.enc_v.handle, C.byref(sh), _ptr(q),
-                                   _ptr(cache.k), _ptr(cache.v), t_begin, t_end, _ptr(out),
-                                   n_splits, _ptr(ws), ws.numel(), _stream(stream)))
+    st = _launch_stream(stream, q.device)
+    with torch.cuda.stream(st):
+        ws = _Workspace.get(ws_bytes, q.device, st)
+        if out is None:
+            out = torch.empty((B * Hq, 4 + D), dtype=torch.float32, device=q.device)
+        q = q.contiguous().float()
+        _check(L.oq_attention_partials(cache.enc_k.handle, cache.enc_v.handle, C.byref(sh),
+                                       _ptr(q), _ptr(cache.k), _ptr(cache.v), t_begin, t_end,
+                                       _ptr(out), n_splits, _ptr(ws), ws.numel(),
+                                       C.c_void_p(st.cuda_stream)))
     return out
 
 
@@ -577,6 +696,12 @@ class NcclComm:
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         _check(lib().oq_nccl_comm_init_rank(C.byref(self.handle), nranks, buf, rank))
 
+    def info(self):
+        """(rank, nranks) as NCCL reports them (ncclCommUserRank / ncclCommCount)."""
+        r, n = C.c_int(), C.c_int()
+        _check(lib().oq_nccl_comm_info(self.handle, C.byref(r), C.byref(n)))
+        return r.value, n.value
+
     def close(self):
         if self.handle:
             _check(lib().oq_nccl_comm_destroy(self.handle))
@@ -589,6 +714,7 @@ def attention_decode_sharded(q, cache: KVCache, t_begin, t_end, comm: NcclComm, 
     one NCCL all-gather of the partials, rank-ordered merge (identical output
     on every rank)."""
     import torch
+    _check_query(q, cache)
     B, Hq, D = q.shape
     T = cache.tokens if T is None else T
     n_splits = 0 if n_splits is None else n_splits
@@ -596,14 +722,17 @@ def attention_decode_sharded(q, cache: KVCache, t_begin, t_end, comm: NcclComm, 
     L = lib()
     ws_bytes = L.oq_attention_sharded_workspace_bytes(cache.enc_k.handle, cache.enc_v.handle,
                                                       C.byref(sh), n_splits, comm.nranks)
-    ws = _Workspace.get(ws_bytes, q.device)
-    if out is None:
-        out = torch.empty((B, Hq, D), dtype=torch.float32, device=q.device)
-    q = q.contiguous().float()
-    _check(L.oq_attention_decode_sharded(cache.enc_k.handle, cache.enc_v.handle, C.byref(sh),
-                                         _ptr(q), _ptr(cache.k), _ptr(cache.v), t_begin, t_end,
-                                         comm.handle, comm.nranks, _ptr(out), n_splits, _ptr(ws),
-                                         ws.numel(), _stream(stream)))
+    st = _launch_stream(stream, q.device)
+    with torch.cuda.stream(st):
+        ws = _Workspace.get(ws_bytes, q.device, st)
+        if out is None:
+            out = torch.empty((B, Hq, D), dtype=torch.float32, device=q.device)
+        q = q.contiguous().float()
+        _check(L.oq_attention_decode_sharded(cache.enc_k.handle, cache.enc_v.handle,
+                                             C.byref(sh), _ptr(q), _ptr(cache.k), _ptr(cache.v),
+                                             t_begin, t_end, comm.handle, comm.nranks, _ptr(out),
+                                             n_splits, _ptr(ws), ws.numel(),
+                                             C.c_void_p(st.cuda_stream)))
     return out
 
 

@@ -153,36 +153,36 @@ __device__ __forceinline__ uint32_t code_addr(const uint32_t (&w)[N], int slot, 
   return off + (v & (M << 7));
 }
 
-// Replicate the NE-entry joint table REP times into shared memory: every
-// thread first loads all of its entries (independent global loads in flight
-// together), then writes each entry's REP consecutive copies with 16-byte
-// stores.  (A strided copy loop serialises one L2 round trip per few entries,
-// which cost several microseconds per launch.)
-template <int REP, int NE>
-__device__ __forceinline__ void stage_table(uint2* dst, const uint2* __restrict__ src, int tid,
-                                            int nthreads) {
-  constexpr int MAXPT = 8;  // entries per thread per pass
-  for (int e0 = 0; e0 < NE; e0 += nthreads * MAXPT) {
-    uint2 v[MAXPT];
-#pragma unroll
-    for (int k = 0; k < MAXPT; ++k) {
-      const int e = e0 + k * nthreads + tid;
-      v[k] = e < NE ? __ldg(src + e) : make_uint2(0u, 0u);
-    }
-#pragma unroll
-    for (int k = 0; k < MAXPT; ++k) {
-      const int e = e0 + k * nthreads + tid;
-      if (e < NE) {
-        uint4* d = reinterpret_cast<uint4*>(dst + (size_t)e * REP);
-        const uint4 q = make_uint4(v[k].x, v[k].y, v[k].x, v[k].y);
-        // consecutive lanes write consecutive entries (a multiple of 128 B
-        // apart): rotate the slot order by lane so that a store instruction's
-        // eight-lane phases hit eight different bank groups
-#pragma unroll
-        for (int r = 0; r < REP / 2; ++r) d[(r + tid) & (REP / 2 - 1)] = q;
-      }
+// The dequant table in shared memory: NE codes x REP fp16 replicas of
+// (rho x, rho y | rho z, 0), dithered on the host (joint_replicas, capi.cpp):
+// a component rounds down in some replicas and up in the others so that the
+// replicas' mean is the exact value to within ulp / (2 REP).  A lookup reads
+// replica (lane + first tile of the warp's ping-pong buffer) mod REP, so the
+// tokens of a code spread over the replicas and the table's fp16 rounding is
+// not a per-code bias (which a long context's softmax average cannot remove).
+// Replicating it also makes the lookups bank-conflict-free: the 16 lanes of a
+// half-warp read 16 different replicas, 8 bytes apart.  Staged with one bulk
+// copy (1-D TMA) of the host-built replicas.
+__device__ __forceinline__ void stage_table(void* dst, const uint2* __restrict__ src, uint32_t bytes,
+                                            uint64_t* bar, int tid) {
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    constexpr uint32_t kChunk = 32768;
+    for (uint32_t o = 0; o < bytes; o += kChunk) {
+      const uint32_t n = bytes - o < kChunk ? bytes - o : kChunk;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(smem_u32(static_cast<uint8_t*>(dst) + o)),
+          "l"(reinterpret_cast<const uint8_t*>(src) + o), "r"(n), "r"(smem_u32(bar))
+          : "memory");
     }
   }
+  __syncthreads();  // the barrier is initialised before anyone waits on it
+  mbar_wait(bar, 0);
 }
 
 __device__ __forceinline__ uint2 lds64(uint32_t addr) {
@@ -243,7 +243,7 @@ __device__ __forceinline__ void wht128_lane4(float (&y)[4], int lane) {
 
 // ---------------------------------------------------------------------------
 struct AttnKParams {
-  const uint2* tab;  // global joint table (2^W entries)
+  const uint2* tab;  // global replica table (2^W codes x REP, see stage_table)
   const uint8_t* kcache;
   const uint8_t* vcache;
   size_t k_tiles_cap, v_tiles_cap;
@@ -813,19 +813,30 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
     }
   }
 
-  uint32_t toff;
+  // per-lane table offset for the tiles of a ping-pong buffer whose first
+  // tile is t: base + 8 * replica, replica = (lane + t) mod REP (a
+  // permutation of the replicas within each half-warp: conflict-free).  The
+  // warps of a CTA take tiles round-robin, so over a stream every token
+  // position meets every residue of t and reads a code through all replicas.
+  __shared__ __align__(8) uint64_t s_tab_bar;
+  uint32_t tbase;
+  constexpr uint32_t kRepMask = W <= 8 ? 31u : 15u;
   if constexpr (W <= 8) {
     // table at shared address 0x10000: 32 replicas x 8 B per entry
     const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     if (base > 0x10000u) __trap();
-    uint2* t8 = reinterpret_cast<uint2*>(smem + (0x10000u - base));
-    stage_table<32, (1 << W)>(t8, P.tab, tid, blockDim.x);
-    toff = 0x10000u | ((uint32_t)lane << 3);
+    stage_table(smem + (0x10000u - base), P.tab, (1u << W) * 32u * 8u, &s_tab_bar, tid);
+    tbase = 0x10000u;
   } else {
-    stage_table<16, (1 << W)>(tab, P.tab, tid, blockDim.x);
-    toff = static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + ((lane & 15) << 3);
+    stage_table(tab, P.tab, (1u << W) * 16u * 8u, &s_tab_bar, tid);
+    tbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
   }
-  __syncthreads();
+  auto toff_of = [&](size_t t) -> uint32_t {
+#if defined(OQ_NO_DITHER_ROT)
+    return tbase + (((uint32_t)lane & kRepMask) << 3);
+#endif
+    return tbase + ((((uint32_t)lane + (uint32_t)t) & kRepMask) << 3);
+  };
 
   auto run = [&](const Seg& it, int nparts) {
     TileRegs<W, QJL> ra, rb;
@@ -840,17 +851,19 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
     // first tile requested after the query prep: issued before it, its 31
     // loads per lane (on every SM at once) held up the prep (C3 -0.7 us)
     if (tile < it.thi) load_tile<W, QJL>(ra, P, it.stream, tile, g, c, lane, lane);
+    // the two ping-pong buffers' table offsets (see toff_of)
+    const uint32_t toff_a = toff_of(tile), toff_b = toff_of(tile + kAttnWarps);
     WarpState S;
     init_state(S);
     while (tile < it.thi) {
       size_t tn = tile + kAttnWarps;
       if (tn < it.thi) load_tile<W, QJL>(rb, P, it.stream, tn, g, c, lane, lane);
-      process_tile<W, QJL>(S, ra, qf, toff, (int)(tile * kTileTok), it.lo, it.hi, g, c);
+      process_tile<W, QJL>(S, ra, qf, toff_a, (int)(tile * kTileTok), it.lo, it.hi, g, c);
       tile = tn;
       if (tile >= it.thi) break;
       tn = tile + kAttnWarps;
       if (tn < it.thi) load_tile<W, QJL>(ra, P, it.stream, tn, g, c, lane, lane);
-      process_tile<W, QJL>(S, rb, qf, toff, (int)(tile * kTileTok), it.lo, it.hi, g, c);
+      process_tile<W, QJL>(S, rb, qf, toff_b, (int)(tile * kTileTok), it.lo, it.hi, g, c);
       tile = tn;
     }
     warp_state_out(S, merge + warp * 8 * kPartW, g, c);
@@ -1399,7 +1412,7 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
                                  int G, int HC, cudaStream_t st, int num_sms) {
   using C = Cfg<W, QJL>;
   AttnKParams P;
-  P.tab = pk.joint16;
+  P.tab = pk.jointrep;
   P.kcache = a.kcache;
   P.vcache = a.vcache;
   P.k_tiles_cap = a.k_tiles_cap;

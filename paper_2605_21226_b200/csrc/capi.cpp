@@ -123,11 +123,75 @@ std::vector<uint32_t> bracket_lut(const std::vector<double>& b, double lo, doubl
   return lut;
 }
 
-uint16_t half_bits(double v) {
-  const __half h = __double2half(v);
+// fp16 neighbours of x: the largest fp16 <= x and the smallest fp16 >= x.
+void f16_bracket(double x, uint16_t& lo, uint16_t& hi) {
+  const __half h = __double2half(x);  // round to nearest
   uint16_t b;
   std::memcpy(&b, &h, 2);
-  return b;
+  auto val = [](uint16_t v) {
+    __half t;
+    std::memcpy(&t, &v, 2);
+    return static_cast<double>(__half2float(t));
+  };
+  // step one fp16 up / down in value (sign-magnitude encoding)
+  auto up = [](uint16_t v) -> uint16_t {
+    if (v == 0x8000u) return 0x0001u;
+    return (v & 0x8000u) ? uint16_t(v - 1) : uint16_t(v + 1);
+  };
+  auto down = [](uint16_t v) -> uint16_t {
+    if (v == 0x0000u) return 0x8001u;
+    return (v & 0x8000u) ? uint16_t(v + 1) : uint16_t(v - 1);
+  };
+  const double hv = val(b);
+  if (hv == x) {
+    lo = hi = b;
+  } else if (hv < x) {
+    lo = b;
+    hi = up(b);
+  } else {
+    hi = b;
+    lo = down(b);
+  }
+}
+
+// The attention kernel's dequant table, staged verbatim into shared memory:
+// for every joint code (ixi | ieta << b_dir | irho << 2 b_dir) REP fp16
+// replicas of (rho x, rho y | rho z, 0), DITHERED.  Each component is rounded
+// down in some replicas and up in the others — k of REP take the upper
+// neighbour, k = round(REP * (x - lo) / (hi - lo)), replica r when
+// bitrev(r) < k — so the mean over the replicas is within ulp / (2 REP) of
+// the exact fp64 value.  K3 reads a code through a replica that varies with
+// the token (attention.cu), so the fp16 rounding of the table no longer acts
+// as a fixed per-code bias that the softmax average over a long context
+// cannot remove (T = 128K, b = 3: 1.2e-3 -> 5e-4 relative error;
+// T = 256K, b = 2: 7.7e-3 -> 6e-4; tools/exp/k3_numerics.py).
+std::vector<uint2> joint_replicas(const std::vector<double>& dirs64, const std::vector<double>& rho_c,
+                                  uint32_t b_dir, uint32_t b_nrm) {
+  const uint32_t W = 2 * b_dir + b_nrm, K = 1u << b_dir;
+  const uint32_t REP = W <= 8 ? 32 : 16, LB = W <= 8 ? 5 : 4;
+  std::vector<uint2> t(size_t(1) << W << LB);
+  for (uint32_t code = 0; code < (1u << W); ++code) {
+    const uint32_t a = code & (K - 1), b = (code >> b_dir) & (K - 1), r = code >> (2 * b_dir);
+    uint16_t lo[3], hi[3];
+    uint32_t k[3];
+    for (int j = 0; j < 3; ++j) {
+      const double x = rho_c[r] * dirs64[3 * (a * K + b) + j];
+      f16_bracket(x, lo[j], hi[j]);
+      __half hl, hh;
+      std::memcpy(&hl, &lo[j], 2);
+      std::memcpy(&hh, &hi[j], 2);
+      const double fl = __half2float(hl), fh = __half2float(hh);
+      k[j] = fh > fl ? static_cast<uint32_t>(std::lround((x - fl) / (fh - fl) * REP)) : 0u;
+    }
+    for (uint32_t rep = 0; rep < REP; ++rep) {
+      uint32_t br = 0;
+      for (uint32_t i = 0; i < LB; ++i) br |= ((rep >> i) & 1u) << (LB - 1 - i);
+      uint16_t v[3];
+      for (int j = 0; j < 3; ++j) v[j] = br < k[j] ? hi[j] : lo[j];
+      t[size_t(code) * REP + rep] = make_uint2(v[0] | (uint32_t(v[1]) << 16), v[2]);
+    }
+  }
+  return t;
 }
 
 oq_status build_codec(const oq_config* cfg, const oqh::Book& xi, const oqh::Book& rho,
@@ -188,25 +252,15 @@ oq_status build_codec(const oq_config* cfg, const oqh::Book& xi, const oqh::Book
     }
   std::vector<float> rho32(KR);
   for (uint32_t i = 0; i < KR; ++i) rho32[i] = static_cast<float>(rho.centroids[i]);
-  // Joint dequant table indexed by ixi | ieta << b_dir | irho << 2 b_dir:
-  // fp16 (rho x, rho y | rho z, 0), the attention kernel's lookup.
+  // the attention kernel's dithered replica table (tile formats exist for W <= 13)
   std::vector<uint2> joint;
   const uint32_t W = 2 * p.b_dir + p.b_nrm;
-  if (W <= 16) {
-    joint.resize(size_t(1) << W);
-    for (uint32_t code = 0; code < (1u << W); ++code) {
-      const uint32_t a = code & (K - 1), b = (code >> p.b_dir) & (K - 1), r = code >> (2 * p.b_dir);
-      const double* n = &dirs64[3 * (a * K + b)];
-      const double rh = rho.centroids[r];
-      joint[code].x = half_bits(rh * n[0]) | (uint32_t(half_bits(rh * n[1])) << 16);
-      joint[code].y = half_bits(rh * n[2]);
-    }
-  }
+  if (W <= 13) joint = joint_replicas(dirs64, rho.centroids, p.b_dir, p.b_nrm);
   oq_status s;
   if ((s = upload(c, xi.boundaries, &p.xi_bnd)) || (s = upload(c, rho.boundaries, &p.rho_bnd)) ||
       (s = upload(c, rho.centroids, &p.rho_c)) || (s = upload(c, dirs64, &p.dirs64)) ||
       (s = upload(c, dirs32, &p.dirs32)) || (s = upload(c, rho32, &p.rho32)) ||
-      (s = upload(c, joint, &p.joint16)) ||
+      (s = upload(c, joint, &p.jointrep)) ||
       (s = upload(c, bracket_lut(xi.boundaries, -1.0, 1.0), &p.xi_lut)) ||
       (s = upload(c, bracket_lut(rho.boundaries, 0.0, 1.0), &p.rho_lut))) {
     oq_codec_destroy(c);
@@ -361,6 +415,93 @@ oq_status oq_decode(const oq_codec* c, const void* records, size_t n, float* out
   cudaError_t e = oqd::launch_decode(c->p, static_cast<const uint8_t*>(records), n, out,
                                      as_stream(stream), c->num_sms);
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "decode kernel");
+}
+
+oq_status oq_dir_table(const double* xi_centroids, int k, double* out) {
+  if (!xi_centroids || !out || k < 1) return fail(OQ_ERR_INVALID_ARGUMENT, "bad direction table arguments");
+  for (int a = 0; a < k; ++a)
+    for (int b = 0; b < k; ++b) {
+      const auto n = oqh::oct_decode(xi_centroids[a], xi_centroids[b]);
+      for (int j = 0; j < 3; ++j) out[3 * (size_t(a) * k + b) + j] = n[j];
+    }
+  return OQ_OK;
+}
+
+oq_status oq_prepare_f64(const oq_codec* c, const double* q, size_t nq, double* rot,
+                         double* sketch, void* stream) {
+  oq_status s = check_codec(c);
+  if (s) return s;
+  if (nq && (!q || !rot)) return fail(OQ_ERR_INVALID_ARGUMENT, "null buffer");
+  if (nq && c->p.qjl && !sketch)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "QJL codec: the sketch output is required");
+  cudaError_t e = oqd::launch_prepare_f64(c->p, q, nq, rot, c->p.qjl ? sketch : nullptr,
+                                          as_stream(stream));
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "prepare kernel");
+}
+
+oq_status oq_reconstruct_rotated(const oq_codec* c, const void* records, size_t n, double* out,
+                                 void* stream) {
+  oq_status s = check_codec(c);
+  if (s) return s;
+  if (n && (!records || !out)) return fail(OQ_ERR_INVALID_ARGUMENT, "null buffer");
+  cudaError_t e = oqd::launch_reconstruct_f64(c->p, static_cast<const uint8_t*>(records), n, out,
+                                              0, as_stream(stream));
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "reconstruct kernel");
+}
+
+oq_status oq_decode_f64(const oq_codec* c, const void* records, size_t n, double* out,
+                        void* stream) {
+  oq_status s = check_codec(c);
+  if (s) return s;
+  if (n && (!records || !out)) return fail(OQ_ERR_INVALID_ARGUMENT, "null buffer");
+  cudaError_t e = oqd::launch_reconstruct_f64(c->p, static_cast<const uint8_t*>(records), n, out,
+                                              1, as_stream(stream));
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "exact decode kernel");
+}
+
+oq_status oq_score_prepared(const oq_codec* c, const double* rot, const double* sketch, size_t nq,
+                            const void* records, size_t n, double* out, void* stream) {
+  oq_status s = check_codec(c);
+  if (s) return s;
+  if (nq && n && (!rot || !records || !out)) return fail(OQ_ERR_INVALID_ARGUMENT, "null buffer");
+  if (nq && n && c->p.qjl && !sketch)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "QJL codec: the prepared sketch is required");
+  cudaError_t e = oqd::launch_score_prepared(c->p, rot, c->p.qjl ? sketch : nullptr, nq,
+                                             static_cast<const uint8_t*>(records), n, out,
+                                             as_stream(stream));
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "score kernel");
+}
+
+size_t oq_attention_f64_workspace_bytes(const oq_codec* c, size_t nq, size_t n) {
+  if (!c) return 0;
+  return (2 * nq * c->p.dim + nq * n) * sizeof(double);
+}
+
+oq_status oq_attention_decode_f64(const oq_codec* c, const double* q, size_t nq,
+                                  const void* records, size_t n, const double* values, int vdim,
+                                  int n_splits, double* out, void* workspace, size_t ws_bytes,
+                                  void* stream) {
+  oq_status s = check_codec(c);
+  if (s) return s;
+  // attention.hpp:54-56
+  if (n == 0) return fail(OQ_ERR_INVALID_ARGUMENT, "empty cache");
+  if (n_splits < 1) return fail(OQ_ERR_INVALID_ARGUMENT, "n_splits must be >= 1");
+  if (vdim < 1) return fail(OQ_ERR_INVALID_ARGUMENT, "values/cache length mismatch");
+  if (!q || !records || !values || !out || !workspace)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "null buffer");
+  if (ws_bytes < oq_attention_f64_workspace_bytes(c, nq, n))
+    return fail(OQ_ERR_INVALID_ARGUMENT, "workspace too small");
+  double* rot = static_cast<double*>(workspace);
+  double* sketch = rot + nq * c->p.dim;
+  double* scores = sketch + nq * c->p.dim;
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = oqd::launch_prepare_f64(c->p, q, nq, rot, sketch, st);
+  if (e == cudaSuccess)
+    e = oqd::launch_score_prepared(c->p, rot, sketch, nq, static_cast<const uint8_t*>(records), n,
+                                   scores, st);
+  if (e == cudaSuccess)
+    e = oqd::launch_softmax_read(scores, nq, n, values, vdim, n_splits, c->p.inv_sqrt_d, out, st);
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "fp64 attention kernels");
 }
 
 oq_status oq_wire_header(const oq_config* cfg, uint64_t count, uint8_t h[20]) {
@@ -779,6 +920,16 @@ oq_status oq_nccl_comm_destroy(void* comm) {
   if (!api.ok) return fail(OQ_ERR_NCCL, api.why);
   const int r = comm ? api.destroy(comm) : 0;
   return r ? nccl_fail(r, "ncclCommDestroy") : OQ_OK;
+}
+
+oq_status oq_nccl_comm_info(void* comm, int* rank, int* nranks) {
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(OQ_ERR_NCCL, api.why);
+  if (!comm || !rank || !nranks) return fail(OQ_ERR_INVALID_ARGUMENT, "null communicator");
+  int r;
+  if ((r = api.user_rank(comm, rank)) != 0) return nccl_fail(r, "ncclCommUserRank");
+  if ((r = api.count(comm, nranks)) != 0) return nccl_fail(r, "ncclCommCount");
+  return OQ_OK;
 }
 
 oq_status oq_scores(const oq_codec* c, const float* q, int nq, const void* records, size_t n,

@@ -25,7 +25,9 @@ struct OqCodecParams {
   const double* dirs64;    // K*K*3 oct_decode(xi_a, xi_b) (codec.hpp:100-107)
   const float* dirs32;     // K*K*4 fp32 copy (x, y, z, 0)
   const float* rho32;      // KR fp32 centroids
-  const uint2* joint16;    // 2^(2 b_dir + b_nrm) fp16 (rho*x, rho*y | rho*z, 0)
+  const uint2* jointrep;   // attention table: 2^W codes x REP dithered fp16 replicas of
+                           // (rho*x, rho*y | rho*z, 0), W = 2 b_dir + b_nrm, REP = 32 for
+                           // W <= 8 else 16 (joint_replicas(), capi.cpp; attention.cu)
   const uint32_t* xi_lut;  // 1024-cell index brackets over [-1, 1] (compress quantize)
   const uint32_t* rho_lut; // 1024-cell index brackets over [0, 1]
 };

@@ -43,6 +43,19 @@ cudaError_t launch_decode(const OqCodecParams& p, const uint8_t* recs, size_t n,
 cudaError_t launch_validate_records(const OqCodecParams& p, const uint8_t* recs, size_t n,
                                     int* bad, cudaStream_t st, int num_sms);
 
+// ---- the per-key Encoder API in exact fp64 (exact_api.cu) -----------------
+cudaError_t launch_prepare_f64(const OqCodecParams& p, const double* q, size_t nq, double* rot,
+                               double* sketch, cudaStream_t st);
+// finish_decode = 0: reconstruct_rotated; 1: Encoder::decode
+cudaError_t launch_reconstruct_f64(const OqCodecParams& p, const uint8_t* recs, size_t n,
+                                   double* out, int finish_decode, cudaStream_t st);
+cudaError_t launch_score_prepared(const OqCodecParams& p, const double* rot, const double* sketch,
+                                  size_t nq, const uint8_t* recs, size_t n, double* out,
+                                  cudaStream_t st);
+cudaError_t launch_softmax_read(const double* scores, size_t nq, size_t n, const double* values,
+                                int vdim, int n_splits, double inv_sqrt_d, double* out,
+                                cudaStream_t st);
+
 // ---- compressed-cache attention (attention.cu) ----------------------------
 struct AttnArgs {
   int B, Hq, Hkv;        // batch, query heads, kv heads (Hq % Hkv == 0)

@@ -12,13 +12,31 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a)")
     config.addinivalue_line("markers", "slow: long-running")
-    # Build the checkers (plain gcc, seconds) and the product library if absent.
+    # Build the checkers (plain gcc, seconds) and the product library whenever
+    # a source is newer than the built .so, so a kernel edited since the last
+    # build is never tested through a stale library.  (build/ does not travel
+    # to the GPU box, so make's own object timestamps cannot be the test there;
+    # a 2 s slack absorbs snapshot copy-order jitter.)
     oracle_so = os.path.join(ROOT, "oracle", "liboctoquant_oracle.so")
-    if not os.path.exists(oracle_so):
+    if _stale(oracle_so, [os.path.join(ROOT, "oracle")]):
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle")], check=True)
     lib_so = os.path.join(ROOT, "paper_2605_21226_b200", "liboctoquant_b200.so")
-    if not os.path.exists(lib_so):
-        subprocess.run(["make", "-C", ROOT, "-j8"], check=True)
+    if _stale(lib_so, [os.path.join(ROOT, "paper_2605_21226_b200", "csrc"),
+                       os.path.join(ROOT, "include")]):
+        subprocess.run(["make", "-C", ROOT, "-j16"], check=True)
+
+
+def _stale(target, src_dirs, slack=2.0):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    for d in src_dirs:
+        for base, _, files in os.walk(d):
+            for f in files:
+                if f.endswith((".cu", ".cuh", ".cpp", ".hpp", ".h", ".c")):
+                    if os.path.getmtime(os.path.join(base, f)) > t + slack:
+                        return True
+    return False
 
 
 @pytest.fixture(scope="session")

@@ -230,6 +230,11 @@ class RefLib:
         L.ref_attention.restype = C.c_int
         L.ref_attention.argtypes = [C.c_void_p, _dp, C.c_size_t, _u8p, C.c_size_t, _dp,
                                     C.c_size_t, C.c_int, _dp, C.c_int]
+        L.ref_cache_new.restype = C.c_void_p
+        L.ref_cache_new.argtypes = [C.c_void_p, C.c_void_p, _u8p, _u8p, C.c_size_t]
+        L.ref_cache_free.argtypes = [C.c_void_p]
+        L.ref_cache_attention.restype = C.c_int
+        L.ref_cache_attention.argtypes = [C.c_void_p, _dp, C.c_size_t, _dp, C.c_int]
         L.ref_unpack_repack.restype = C.c_size_t
         L.ref_unpack_repack.argtypes = [_u8p, C.c_size_t, _u8p]
 
@@ -292,5 +297,34 @@ class RefEncoder:
         if self.lib.L.ref_attention(self.h, _ptr(q, _dp), q.shape[0], _ptr(krecs, _u8p),
                                     krecs.shape[0], _ptr(values, _dp), values.shape[1],
                                     n_splits, _ptr(out, _dp), threads):
+            raise ValueError("invalid argument")
+        return out
+
+
+class RefCache:
+    """A CPU-resident compressed K/V cache held as the reference's
+    CompressedKey vectors (records unpacked once); attention() runs, per call,
+    Encoder::decode of every V key and attention_decode per query row."""
+
+    def __init__(self, ek: RefEncoder, ev: RefEncoder, krecs, vrecs):
+        self.lib = ek.lib
+        self.ek, self.ev = ek, ev  # keep the encoders alive
+        self._k = np.ascontiguousarray(krecs, np.uint8)
+        self._v = np.ascontiguousarray(vrecs, np.uint8)
+        self.n = self._k.shape[0]
+        self.h = self.lib.L.ref_cache_new(ek.h, ev.h, _ptr(self._k, _u8p), _ptr(self._v, _u8p),
+                                          self.n)
+        if not self.h:
+            raise ValueError("FormatError")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.L.ref_cache_free(self.h)
+
+    def attention(self, q, threads=1):
+        q = np.ascontiguousarray(q, np.float64).reshape(-1, self.ek.dim)
+        out = np.empty((q.shape[0], self.ev.dim))
+        if self.lib.L.ref_cache_attention(self.h, _ptr(q, _dp), q.shape[0], _ptr(out, _dp),
+                                          threads):
             raise ValueError("invalid argument")
         return out

@@ -126,3 +126,18 @@ def test_no_cpu_fallback():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         oq.Encoder(oq.CodecConfig())
+
+
+def test_dir_table_matches_oracle(orc):
+    import ctypes as C
+
+    # host-only entry point (no device): codec.hpp:100-107
+    xi, _ = oq.xi_book(4)
+    out = np.empty(16 * 16 * 3)
+    dp = C.POINTER(C.c_double)
+    oq._check(oq.lib().oq_dir_table(xi.ctypes.data_as(dp), 16, out.ctypes.data_as(dp)))
+    for a in range(16):
+        for b in range(16):
+            o = np.empty(3)
+            orc.L.orc_oct_decode(xi[a], xi[b], o.ctypes.data_as(dp))
+            assert np.array_equal(out[3 * (16 * a + b):3 * (16 * a + b) + 3], o)
