@@ -202,8 +202,10 @@ oq_status oq_attention_decode(const oq_codec* ck, const oq_codec* cv, const oq_a
                               void* stream);
 /* Sequence sharding: the SoftmaxState (m, l, acc) of tokens [t_begin, t_end)
  * per (b, q head) -> partial [B*Hq][4 + dim] fp32 = (m, l, 0, 0, acc[dim]),
- * m being the running max of log2-scaled logits and acc in the rotated V
- * frame.  Chunks merge with oq_attention_combine in token order, which is
+ * m the reference point l and acc are scaled to (logits in log2 units: the
+ * running max, or for 2-bit tiles up to 2 below it — the kernel skips
+ * rescales of small max moves; the triple stays exact either way) and acc in
+ * the rotated V frame.  Chunks merge with oq_attention_combine in token order, which is
  * the reference's SoftmaxState::merge (attention.hpp:36-44). */
 oq_status oq_attention_partials(const oq_codec* ck, const oq_codec* cv,
                                 const oq_attn_shape* shape, const float* q, const void* kcache,

@@ -19,7 +19,9 @@ ncucodec)
   ;;
 ncu)
   timeout 600 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-other-configs > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?" >> gpurun_out/ncu_launch.log
-  timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:attn_partials -s 4 -c 1 -o gpurun_out/prof_attn -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-compress --no-other-configs > gpurun_out/ncu_attn.log 2>&1; echo "ncu attn rc=$?" >> gpurun_out/ncu_attn.log
+  for cfg in c3 c4 c5; do
+    timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:attn_partials -s 4 -c 1 -o gpurun_out/prof_attn_$cfg -f python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu-baseline --no-compress --no-other-configs > gpurun_out/ncu_attn_$cfg.log 2>&1; echo "ncu attn $cfg rc=$?" >> gpurun_out/ncu_attn_$cfg.log
+  done
   timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:"compress_fast_kernel|compress_fixup_kernel|decode128_kernel" -s 3 -c 3 -o gpurun_out/prof_codec -f python tools/codec_kernels.py 3 > gpurun_out/ncu_codec.log 2>&1; echo "ncu codec rc=$?" >> gpurun_out/ncu_codec.log
   ;;
 esac; done

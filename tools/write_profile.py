@@ -21,13 +21,15 @@ def main():
     g = os.path.join(ROOT, "gpurun_out")
     d = json.loads([x for x in open(os.path.join(g, "bench.log")) if x.startswith("{")][-1])
     tr = {}
-    for rep in ("prof_attn.ncu-rep", "prof_codec.ncu-rep"):
-        tr.update(json.loads(run("traffic", os.path.join(g, rep))))
+    for rep in ("prof_attn_c3.ncu-rep", "prof_attn_c4.ncu-rep", "prof_attn_c5.ncu-rep",
+                "prof_codec.ncu-rep"):
+        if os.path.exists(os.path.join(g, rep)):
+            tr.update(json.loads(run("traffic", os.path.join(g, rep))))
     json.dump({"source": f"ncu --set full --clock-control none, profiles/{name}_summary.md",
                "dram_bytes_per_launch": tr},
               open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
     r, c = d["roofline"], d["compress"]
-    att = [k for k in tr if k.startswith("attn_partials")][0]
+    att = "attn_partials_kernel<10, 0, 8>"
     pyt = [x for x in open(os.path.join(g, "pytest_gpu.log")) if "passed" in x]
     out = [f"# {name} — {note}\n",
            "Command: `STAGES=\"smoke pytest bench ncu\" bash tools/gpu_round.sh`.  smoke ok; "
@@ -58,9 +60,14 @@ def main():
                    f"({100 * v['decode_frac_of_hbm']:.1f} %) |")
     out.append("\n## Launch list (`ncu --metrics gpu__time_duration.sum`)\n")
     out.append(run("launches", os.path.join(g, "launches.csv")))
-    out.append("## K3, `ncu --set full`\n")
-    out.append(run("full", os.path.join(g, "prof_attn.ncu-rep"), "--units", "131072", "--unit-name",
-                   "tile"))
+    # tiles per launch: B * Hkv * T / 32 (one 8-head chunk per stream at G = 7)
+    for cfg, tiles, what in (("c3", 8 * 4 * 131072 // 32, "C3: B=8, T=128K, 3-bit"),
+                             ("c4", 32 * 4 * 32768 // 32, "C4: B=32, T=32K, QJL 2-bit K"),
+                             ("c5", 8 * 4 * (1 << 20) // 32, "C5 at P = 1: B=8, T=1M, 2-bit")):
+        rep = os.path.join(g, f"prof_attn_{cfg}.ncu-rep")
+        if os.path.exists(rep):
+            out.append(f"## K3, `ncu --set full` — {what}\n")
+            out.append(run("full", rep, "--units", str(tiles), "--unit-name", "tile"))
     out.append("## K1 (certified-fp32 pass + exact re-rounding of the undecided triplets) and K2, "
                "`ncu --set full` (2^20 keys, b=3)\n")
     out.append(run("full", os.path.join(g, "prof_codec.ncu-rep")))
