@@ -163,8 +163,8 @@ __device__ __forceinline__ uint32_t code_addr(const uint32_t (&w)[N], int slot, 
 // Replicating it also makes the lookups bank-conflict-free: the 16 lanes of a
 // half-warp read 16 different replicas, 8 bytes apart.  Staged with one bulk
 // copy (1-D TMA) of the host-built replicas.
-__device__ __forceinline__ void stage_table(void* dst, const uint2* __restrict__ src, uint32_t bytes,
-                                            uint64_t* bar, int tid) {
+__device__ __forceinline__ void stage_table_issue(void* dst, const uint2* __restrict__ src,
+                                                  uint32_t bytes, uint64_t* bar, int tid) {
   if (tid == 0) {
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -181,8 +181,6 @@ __device__ __forceinline__ void stage_table(void* dst, const uint2* __restrict__
           : "memory");
     }
   }
-  __syncthreads();  // the barrier is initialised before anyone waits on it
-  mbar_wait(bar, 0);
 }
 
 __device__ __forceinline__ uint2 lds64(uint32_t addr) {
@@ -426,9 +424,13 @@ __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL
   // the first two V groups' lookups do not depend on the softmax: issue them
   // before it so their latency overlaps the max/rescale chain (one group:
   // C3/C5/C4 -0.3/-0.8/0 %, two: a further -0/-0.4/-1.3 %, three: slower)
+#ifndef OQ_PREV_QJL
+#define OQ_PREV_QJL 2
+#endif
+  constexpr int kPreV = QJL ? OQ_PREV_QJL : 2;  // V groups issued before the softmax
   uint2 e0[2][2][4];
 #pragma unroll
-  for (int gg = 0; gg < 2; ++gg)
+  for (int gg = 0; gg < kPreV; ++gg)
 #pragma unroll
     for (int uu = 0; uu < 2; ++uu)
 #pragma unroll
@@ -491,7 +493,7 @@ __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL
       for (int uu = 0; uu < 2; ++uu)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          e[uu][q] = (kk == 0 && grp < 2)
+          e[uu][q] = (kk == 0 && grp < kPreV)
                          ? e0[grp < 2 ? grp : 0][uu][q]
                          : lds64(code_addr<W>(R.vc, (2 * grp + uu) * 8 + 4 * kk + q, toff));
 #pragma unroll
@@ -791,8 +793,30 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, c = lane & 3;
 
-  // the first segment's q row of this warp's head, requested before the
-  // table staging so its latency is hidden behind it
+  // Programmatic dependent launch: let the next launch in the stream start
+  // its CTAs (they can only become resident as ours exit), and stage the
+  // dequant table — the codec's constant, written by no earlier kernel — before
+  // waiting for the previous grid; everything after griddepcontrol.wait
+  // (q, seq_lens, the caches, the workspace counters and partials) sees its
+  // writes.  Without the launch attribute both instructions are no-ops.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  __shared__ __align__(8) uint64_t s_tab_bar;
+  uint32_t tbase;
+  constexpr uint32_t kRepMask = W <= 8 ? 31u : 15u;
+  if constexpr (W <= 8) {
+    // table at shared address 0x10000: 32 replicas x 8 B per entry
+    const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    if (base > 0x10000u) __trap();
+    stage_table_issue(smem + (0x10000u - base), P.tab, (1u << W) * 32u * 8u, &s_tab_bar, tid);
+    tbase = 0x10000u;
+  } else {
+    stage_table_issue(tab, P.tab, (1u << W) * 16u * 8u, &s_tab_bar, tid);
+    tbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  // the first segment's q row of this warp's head, requested while the table
+  // arrives so its latency is hidden behind it
   int sh_pre = -1;
   float4 q_pre = make_float4(0.f, 0.f, 0.f, 0.f);
   // (not with QJL: the extra live float4 makes that variant spill in its tile loop)
@@ -812,25 +836,14 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
                       lane);
     }
   }
+  __syncthreads();  // the table's barrier is initialised before anyone waits on it
+  mbar_wait(&s_tab_bar, 0);
 
   // per-lane table offset for the tiles of a ping-pong buffer whose first
   // tile is t: base + 8 * replica, replica = (lane + t) mod REP (a
   // permutation of the replicas within each half-warp: conflict-free).  The
   // warps of a CTA take tiles round-robin, so over a stream every token
   // position meets every residue of t and reads a code through all replicas.
-  __shared__ __align__(8) uint64_t s_tab_bar;
-  uint32_t tbase;
-  constexpr uint32_t kRepMask = W <= 8 ? 31u : 15u;
-  if constexpr (W <= 8) {
-    // table at shared address 0x10000: 32 replicas x 8 B per entry
-    const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-    if (base > 0x10000u) __trap();
-    stage_table(smem + (0x10000u - base), P.tab, (1u << W) * 32u * 8u, &s_tab_bar, tid);
-    tbase = 0x10000u;
-  } else {
-    stage_table(tab, P.tab, (1u << W) * 16u * 8u, &s_tab_bar, tid);
-    tbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
-  }
   auto toff_of = [&](size_t t) -> uint32_t {
 #if defined(OQ_NO_DITHER_ROT)
     return tbase + (((uint32_t)lane & kRepMask) << 3);
@@ -1468,8 +1481,23 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
   }
   cudaError_t e = set_smem_once(attn_partials_kernel<W, QJL, NW>, C::smem(NW));
   if (e != cudaSuccess) return e;
-  attn_partials_kernel<W, QJL, NW><<<grid, NW * 32, C::smem(NW), st>>>(P);
-  return cudaGetLastError();
+  // programmatic dependent launch (see the kernel's prologue): the table
+  // staging overlaps the previous kernel's tail (OQ_ATTN_PDL=0 disables it)
+  static const bool pdl = [] {
+    const char* v = getenv("OQ_ATTN_PDL");
+    return !(v && v[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = C::smem(NW);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, attn_partials_kernel<W, QJL, NW>, P);
 }
 
 cudaError_t launch_qprep(const OqCodecParams& pk, const AttnArgs& a, cudaStream_t st) {
