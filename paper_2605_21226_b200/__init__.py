@@ -34,7 +34,8 @@ from dataclasses import dataclass
 import numpy as np
 
 __all__ = [
-    "CodecConfig", "Encoder", "FormatError", "KVCache", "ROUNDINGS", "attention_decode",
+    "AttentionPipeline", "CodecConfig", "Encoder", "FormatError", "KVCache", "ROUNDINGS",
+    "attention_decode",
     "attention_decode_dense",
     "attention_partials", "attention_combine", "default_bit_split",
     "effective_bits_per_coord", "lib", "pack_keys", "parse_rounding", "record_bytes", "rho_book",
@@ -624,6 +625,65 @@ def attention_decode(q, cache: KVCache, n_splits=None, seq_lens=None, T=None, ou
                                      _ptr(q), _ptr(cache.k), _ptr(cache.v), _ptr(out), n_splits,
                                      _ptr(ws), ws.numel(), C.c_void_p(st.cuda_stream)))
     return out
+
+
+class AttentionPipeline:
+    """Serving loop for attention_decode with HOST queries and outputs.
+
+    Each ``run(q_host, out_host)`` copies that step's queries host -> device,
+    runs the fused attention and copies the output device -> host, on three
+    streams with double-buffered device q / out, so step i+1's upload and step
+    i's download overlap the attention kernels instead of serialising with
+    them on one stream.  q_host / out_host: pinned CPU float32 [B, Hq, dim];
+    out_host is complete once ``synchronize()`` (or the step's event from
+    ``run``) has passed.  Every step still moves its own inputs and outputs.
+    """
+
+    def __init__(self, cache: KVCache, Hq, n_splits=0, seq_lens=None, device=None):
+        import torch
+        self.cache, self.Hq, self.n_splits, self.seq_lens = cache, Hq, n_splits, seq_lens
+        dev = device if device is not None else cache.k.device
+        D = cache.enc_k.cfg.dim
+        self.dev = dev
+        self.q = [torch.empty((cache.B, Hq, D), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.out = [torch.empty((cache.B, Hq, D), dtype=torch.float32, device=dev)
+                    for _ in range(2)]
+        self.compute = torch.cuda.Stream(device=dev)
+        self.h2d = torch.cuda.Stream(device=dev)
+        self.d2h = torch.cuda.Stream(device=dev)
+        self.q_ready = [torch.cuda.Event() for _ in range(2)]
+        self.q_free = [torch.cuda.Event() for _ in range(2)]
+        self.out_ready = [torch.cuda.Event() for _ in range(2)]
+        self.out_free = [torch.cuda.Event() for _ in range(2)]
+        self.done = [torch.cuda.Event() for _ in range(2)]
+        self.i = 0
+        for e in self.q_free + self.out_free:  # both buffers start free
+            e.record(self.compute)
+
+    def run(self, q_host, out_host):
+        import torch
+        j = self.i & 1
+        self.i += 1
+        with torch.cuda.stream(self.h2d):
+            self.h2d.wait_event(self.q_free[j])      # step i-2's kernel has read q[j]
+            self.q[j].copy_(q_host, non_blocking=True)
+            self.q_ready[j].record(self.h2d)
+        self.compute.wait_event(self.q_ready[j])
+        self.compute.wait_event(self.out_free[j])    # step i-2's download of out[j] is done
+        attention_decode(self.q[j], self.cache, n_splits=self.n_splits, seq_lens=self.seq_lens,
+                         out=self.out[j], stream=self.compute)
+        self.q_free[j].record(self.compute)
+        self.out_ready[j].record(self.compute)
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_event(self.out_ready[j])
+            out_host.copy_(self.out[j], non_blocking=True)
+            self.out_free[j].record(self.d2h)
+            self.done[j].record(self.d2h)
+        return self.done[j]
+
+    def synchronize(self):
+        for s in (self.h2d, self.compute, self.d2h):
+            s.synchronize()
 
 
 def attention_decode_dense(enc: Encoder, q, records, values, n_splits=1, stream=None):

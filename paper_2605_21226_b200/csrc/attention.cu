@@ -35,7 +35,7 @@ namespace oqd {
 
 constexpr int kTileTok = 32;
 constexpr int kNT = 43;  // triplets at dim 128
-constexpr int kAttnWarpsMax = 16;
+constexpr int kMaxSmem = 227 * 1024 - 2048;  // dynamic smem per CTA (227 KB, static part reserved)
 constexpr int kPartW = 132;  // (m, l, 0, 0, acc[128]): acc 16-byte aligned
 
 // ---------------------------------------------------------------------------
@@ -281,7 +281,14 @@ struct Cfg {
   // TAB_BYTES then spans from the start of dynamic smem to its end
   static constexpr int TAB_BYTES = W <= 8 ? 0x10000 + (1 << W) * 256 : (1 << W) * 16 * 8;
   static constexpr int QS_FLOATS = 8 * 2 * 129;  // fused query prep scratch
-  static constexpr int smem(int nw) { return TAB_BYTES + nw * 8 * kPartW * 4 + QS_FLOATS * 4; }
+  // per-warp region: the merge slot (8 heads x kPartW floats) and, with a
+  // TMA ring of `ring` stages, the staged tiles (aliased: the ring is idle
+  // when the warp writes its merge slot)
+  static constexpr int STAGE = KTILE + VTILE;
+  static constexpr int wreg(int ring) {
+    return (ring * STAGE > 8 * kPartW * 4 ? ring * STAGE : 8 * kPartW * 4);
+  }
+  static constexpr int smem(int nw, int ring = 0) { return TAB_BYTES + nw * wreg(ring) + QS_FLOATS * 4; }
 };
 
 template <int W, bool QJL>
@@ -333,6 +340,51 @@ __device__ __forceinline__ void load_tile(TileRegs<W, QJL>& r, const AttnKParams
     r.gr = __ldg(reinterpret_cast<const uint2*>(qa) + g);
     r.sg = __ldg(reinterpret_cast<const uint4*>(qa + 64) + (4 * g + c));
   }
+}
+
+// The same register image from a tile staged verbatim in shared memory (the
+// TMA ring): identical word offsets, LDS instead of LDG.
+template <int W, bool QJL>
+__device__ __forceinline__ void load_tile_smem(TileRegs<W, QJL>& r, const uint8_t* kt,
+                                               const uint8_t* vt, int g, int c, int kl, int vl) {
+  using C = Cfg<W, QJL>;
+  r.gk = reinterpret_cast<const float4*>(kt)[g];
+  r.gv = reinterpret_cast<const float4*>(vt)[g];
+  const uint32_t* kw = reinterpret_cast<const uint32_t*>(kt + 128);
+  const uint32_t* vw = reinterpret_cast<const uint32_t*>(vt + 128);
+#pragma unroll
+  for (int i = 0; i < C::KWF; ++i)
+    r.kc[i] = i < C::KW3 ? kw[32 * i + kl]
+                         : (c < 3 ? kw[32 * C::KW3 + 24 * (i - C::KW3) + 3 * g + c] : 0u);
+#pragma unroll
+  for (int i = 0; i < C::VWF; ++i)
+    r.vc[i] = i < C::VW7 ? vw[32 * i + vl] : (g < 7 ? vw[32 * C::VW7 + 28 * (i - C::VW7) + vl] : 0u);
+  if (QJL) {
+    const uint8_t* qa = kt + 128 + 4 * C::KCODE;
+    r.gr = reinterpret_cast<const uint2*>(qa)[g];
+    r.sg = reinterpret_cast<const uint4*>(qa + 64)[4 * g + c];
+  }
+}
+
+// One TMA ring stage <- tile `tile` of `stream`: the K and V tiles, 1-D bulk
+// copies completing on the stage's mbarrier.  Called by one lane.
+template <int W, bool QJL>
+__device__ __forceinline__ void ring_issue(uint8_t* stage, uint64_t* bar, const AttnKParams& P,
+                                           size_t stream, size_t tile) {
+  using C = Cfg<W, QJL>;
+  const uint8_t* kt = P.kcache + (stream * P.k_tiles_cap + tile) * (size_t)C::KTILE;
+  const uint8_t* vt = P.vcache + (stream * P.v_tiles_cap + tile) * (size_t)C::VTILE;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"((uint32_t)(C::KTILE + C::VTILE))
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(stage)), "l"(kt), "r"((uint32_t)C::KTILE), "r"(smem_u32(bar))
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(stage + C::KTILE)), "l"(vt), "r"((uint32_t)C::VTILE), "r"(smem_u32(bar))
+      : "memory");
 }
 
 // Online-softmax state of one warp for its 8 heads (2 per lane).
@@ -627,19 +679,19 @@ __device__ __forceinline__ void warp_state_out(WarpState& S, float* mw, int g, i
 template <int NW>
 __device__ __forceinline__ void merge_store(const AttnKParams& P, const Seg& it,
                                             const float* merge, float* mf, int tid,
-                                            int nthreads) {
+                                            int nthreads, int ws) {
   const float NEG_INF = -__int_as_float(0x7f800000);
   const int nh = min(8, P.G - 8 * it.hc);
   if (tid < nh) {
     float M = NEG_INF;
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
-      const float* mm = merge + (w * 8 + tid) * kPartW;
+      const float* mm = merge + w * ws + tid * kPartW;
       if (mm[1] > 0.f) M = fmaxf(M, mm[0]);
     }
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
-      const float* mm = merge + (w * 8 + tid) * kPartW;
+      const float* mm = merge + w * ws + tid * kPartW;
       mf[w * 8 + tid] = mm[1] > 0.f ? ex2(mm[0] - M) : 0.f;
     }
     mf[NW * 8 + tid] = M;
@@ -652,7 +704,7 @@ __device__ __forceinline__ void merge_store(const AttnKParams& P, const Seg& it,
       v = mf[NW * 8 + h];
     } else if (j == 1 || j >= 4) {
 #pragma unroll
-      for (int w = 0; w < NW; ++w) v += merge[(w * 8 + h) * kPartW + j] * mf[w * 8 + h];
+      for (int w = 0; w < NW; ++w) v += merge[w * ws + h * kPartW + j] * mf[w * 8 + h];
     }
     const size_t row = (size_t)it.b * P.Hq + (size_t)it.kvh * P.G + 8 * it.hc + h;
     P.partials[(row * P.n_parts + it.part) * kPartW + j] = v;
@@ -781,13 +833,23 @@ __device__ __forceinline__ void combine_row(const float* base, int n, float* out
 
 // Variant A: each warp streams its tiles from HBM straight into registers,
 // prefetching one tile ahead (ping-pong register images).
-template <int W, bool QJL, int kAttnWarps>
+// RING = 0: each warp prefetches the next tile into registers (ping-pong
+// register images).  RING > 0: each warp owns a RING-stage ring of tiles in
+// shared memory filled by 1-D TMA (cp.async.bulk) RING tiles ahead; a tile's
+// words move to registers with LDS when it is processed (one register image,
+// so more warps fit per SM).
+template <int W, bool QJL, int kAttnWarps, int RING = 0>
 __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const AttnKParams P) {
   using C = Cfg<W, QJL>;
+  constexpr int WREG = C::wreg(RING);   // bytes per warp region
+  constexpr int WS = WREG / 4;          // ... in floats (merge slot stride)
   uint8_t* smem = g_attn_smem;
   uint2* tab = reinterpret_cast<uint2*>(smem);
   float* merge = reinterpret_cast<float*>(smem + C::TAB_BYTES);
-  float* qs = merge + kAttnWarps * 8 * kPartW;
+  uint8_t* ring = smem + C::TAB_BYTES;  // warp w: ring + w * WREG (aliases its merge slot)
+  float* qs = reinterpret_cast<float*>(smem + C::TAB_BYTES + kAttnWarps * WREG);
+  __shared__ __align__(8) uint64_t s_ring_bar[kAttnWarps][RING > 0 ? RING : 1];
+  uint32_t ring_phase = 0;  // bit s: parity of the next completion of stage s
   __shared__ int s_last;
   __shared__ float s_mf[(kAttnWarps + 1) * 8];  // merge_store scale factors
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -836,6 +898,11 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
                       lane);
     }
   }
+  if constexpr (RING > 0) {
+    if (lane == 0)
+      for (int st = 0; st < RING; ++st) mbar_init(&s_ring_bar[warp][st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();  // the table's barrier is initialised before anyone waits on it
   mbar_wait(&s_tab_bar, 0);
 
@@ -853,6 +920,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
 
   auto run = [&](const Seg& it, int nparts) {
     TileRegs<W, QJL> ra, rb;
+    (void)ra;
+    (void)rb;
     size_t tile = it.tlo + warp;
     uint32_t qf[C::QF];
     if (P.fuse) {
@@ -861,12 +930,42 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
     } else {
       load_qfrag(qf, P, it.sh, lane);
     }
+    WarpState S;
+    if constexpr (RING > 0) {
+      uint8_t* wr = ring + warp * WREG;
+      // the first RING tiles of this warp, issued after the query prep (the
+      // proxy fence orders the region's earlier generic stores — the merge
+      // slot it aliases — before the TMA writes)
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (lane == 0)
+#pragma unroll
+        for (int st = 0; st < RING; ++st) {
+          const size_t t = tile + (size_t)st * kAttnWarps;
+          if (t < it.thi) ring_issue<W, QJL>(wr + st * C::STAGE, &s_ring_bar[warp][st], P, it.stream, t);
+        }
+      init_state(S);
+      int st = 0;
+      while (tile < it.thi) {
+        mbar_wait(&s_ring_bar[warp][st], (ring_phase >> st) & 1u);
+        ring_phase ^= 1u << st;
+        TileRegs<W, QJL> r;
+        load_tile_smem<W, QJL>(r, wr + st * C::STAGE, wr + st * C::STAGE + C::KTILE, g, c, lane,
+                               lane);
+        __syncwarp();  // every lane has its words: the stage can be refilled
+        const size_t tn = tile + (size_t)RING * kAttnWarps;
+        if (lane == 0 && tn < it.thi)
+          ring_issue<W, QJL>(wr + st * C::STAGE, &s_ring_bar[warp][st], P, it.stream, tn);
+        process_tile<W, QJL>(S, r, qf, toff_of(tile), (int)(tile * kTileTok), it.lo, it.hi, g, c);
+        tile += kAttnWarps;
+        st = st + 1 == RING ? 0 : st + 1;
+      }
+      __syncwarp();
+    } else {
     // first tile requested after the query prep: issued before it, its 31
     // loads per lane (on every SM at once) held up the prep (C3 -0.7 us)
     if (tile < it.thi) load_tile<W, QJL>(ra, P, it.stream, tile, g, c, lane, lane);
     // the two ping-pong buffers' table offsets (see toff_of)
     const uint32_t toff_a = toff_of(tile), toff_b = toff_of(tile + kAttnWarps);
-    WarpState S;
     init_state(S);
     while (tile < it.thi) {
       size_t tn = tile + kAttnWarps;
@@ -879,9 +978,10 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
       process_tile<W, QJL>(S, rb, qf, toff_b, (int)(tile * kTileTok), it.lo, it.hi, g, c);
       tile = tn;
     }
-    warp_state_out(S, merge + warp * 8 * kPartW, g, c);
+    }
+    warp_state_out(S, merge + warp * WS, g, c);
     __syncthreads();
-    merge_store<kAttnWarps>(P, it, merge, s_mf, tid, blockDim.x);
+    merge_store<kAttnWarps>(P, it, merge, s_mf, tid, blockDim.x, WS);
     if (P.fuse) {
       // the CTA that lands a stream's last partial finalises its rows.  The
       // barrier orders the CTA's partial stores before thread 0's gpu-scope
@@ -1420,7 +1520,7 @@ cudaError_t launch_pack_tiles(const OqCodecParams& p, int role, const uint8_t* r
   return cudaGetLastError();
 }
 
-template <int W, bool QJL, int NW>
+template <int W, bool QJL, int NW, int RING = 0>
 static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int splits,
                                  int G, int HC, cudaStream_t st, int num_sms) {
   using C = Cfg<W, QJL>;
@@ -1479,7 +1579,7 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
     const size_t U = (size_t)P.n_sh * P.tps;
     grid = (int)(U < (size_t)num_sms ? (U ? U : 1) : num_sms);
   }
-  cudaError_t e = set_smem_once(attn_partials_kernel<W, QJL, NW>, C::smem(NW));
+  cudaError_t e = set_smem_once(attn_partials_kernel<W, QJL, NW, RING>, C::smem(NW, RING));
   if (e != cudaSuccess) return e;
   // programmatic dependent launch (see the kernel's prologue): the table
   // staging overlaps the previous kernel's tail (OQ_ATTN_PDL=0 disables it)
@@ -1490,14 +1590,14 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NW * 32);
-  cfg.dynamicSmemBytes = C::smem(NW);
+  cfg.dynamicSmemBytes = C::smem(NW, RING);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, attn_partials_kernel<W, QJL, NW>, P);
+  return cudaLaunchKernelEx(&cfg, attn_partials_kernel<W, QJL, NW, RING>, P);
 }
 
 cudaError_t launch_qprep(const OqCodecParams& pk, const AttnArgs& a, cudaStream_t st) {
@@ -1525,17 +1625,29 @@ cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecPara
                                       int num_sms) {
   const int G = a.Hq / a.Hkv, HC = (G + 7) / 8;
   const int W = 2 * pk.b_dir + pk.b_nrm;
-  // Warps per CTA (one CTA per SM): OQ_ATTN_WARPS selects a variant for
-  // tuning runs; the default is the measured best.
-  static const int nw = [] {
-    const char* e = getenv("OQ_ATTN_WARPS");
-    const int v = e ? atoi(e) : 8;
-    return (v == 8 || v == 12) ? v : 8;
+  // Warps per CTA (one CTA per SM) and the tile delivery: OQ_ATTN_WARPS /
+  // OQ_ATTN_RING select a variant for tuning runs; the default is the
+  // measured best.  RING 0 = register ping-pong, 2 / 3 = TMA ring stages.
+  static const int ring_env = [] {
+    const char* e = getenv("OQ_ATTN_RING");
+    return e ? atoi(e) : -1;
   }();
-#define OQ_LAUNCH(WW, QQ)                                                              \
-  if (W == WW && (bool)pk.qjl == QQ) {                                                \
-    if (nw == 12) return launch_attn_t<WW, QQ, 12>(pk, a, splits, G, HC, st, num_sms); \
-    return launch_attn_t<WW, QQ, 8>(pk, a, splits, G, HC, st, num_sms);               \
+  static const int nw_env = [] {
+    const char* e = getenv("OQ_ATTN_WARPS");
+    return e ? atoi(e) : -1;
+  }();
+  // measured defaults (tools/exp/abn.sh, r02): the byte-coded 2-bit tiles
+  // (W = 7, C4/C5) run 12 warps fed by a 2-stage TMA ring (C4 -10 %, C5
+  // -1.7 %); the 10-bit tiles (C3) keep 8 warps with register prefetch (the
+  // ring costs them 2-10 %)
+  const int ring = ring_env >= 0 ? ring_env : (W == 7 ? 2 : 0);
+  const int nw = nw_env > 0 ? nw_env : (ring ? 12 : 8);
+#define OQ_LAUNCH(WW, QQ)                                                                   \
+  if (W == WW && (bool)pk.qjl == QQ) {                                                     \
+    if (ring == 3 && nw == 12 && Cfg<WW, QQ>::smem(12, 3) <= kMaxSmem) return launch_attn_t<WW, QQ, 12, 3>(pk, a, splits, G, HC, st, num_sms); \
+    if (ring >= 2 && nw == 12 && Cfg<WW, QQ>::smem(12, 2) <= kMaxSmem) return launch_attn_t<WW, QQ, 12, 2>(pk, a, splits, G, HC, st, num_sms); \
+    if (ring >= 2 && Cfg<WW, QQ>::smem(8, 2) <= kMaxSmem) return launch_attn_t<WW, QQ, 8, 2>(pk, a, splits, G, HC, st, num_sms);  \
+    return launch_attn_t<WW, QQ, 8, 0>(pk, a, splits, G, HC, st, num_sms);                 \
   }
   OQ_LAUNCH(10, false)
   OQ_LAUNCH(10, true)

@@ -170,3 +170,21 @@ def test_long_context_weighted_stream_k(orc, cuda):
     out = oq.attention_combine(d["cache"].enc_v, parts, rows, 2, 132, rows * 132)
     full = oq.attention_decode(q, d["cache"]).cpu().numpy()
     assert rel_err(out.reshape(B, Hq, 128).cpu().numpy(), full).max() <= TOL
+
+
+def test_attention_pipeline_host_buffers(orc, cuda):
+    """AttentionPipeline (host q in, host out back, copies on their own
+    streams): every step's output equals attention_decode on the device."""
+    import torch
+    B, Hq, Hkv, T = 2, 14, 2, 3000
+    d = build(orc, cuda, B, Hq, Hkv, T, seed=11)
+    pipe = oq.AttentionPipeline(d["cache"], Hq)
+    g = torch.Generator().manual_seed(3)
+    qs = [torch.randn((B, Hq, 128), generator=g).pin_memory() for _ in range(5)]
+    outs = [torch.empty((B, Hq, 128)).pin_memory() for _ in range(5)]
+    for qh, oh in zip(qs, outs):
+        pipe.run(qh, oh)
+    pipe.synchronize()
+    for qh, oh in zip(qs, outs):
+        want = oq.attention_decode(qh.to(cuda), d["cache"]).cpu()
+        assert torch.equal(oh, want)

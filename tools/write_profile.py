@@ -29,7 +29,7 @@ def main():
                "dram_bytes_per_launch": tr},
               open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
     r, c = d["roofline"], d["compress"]
-    att = "attn_partials_kernel<10, 0, 8>"
+    att = [k for k in tr if k.startswith("attn_partials_kernel<10, 0,")][0]
     pyt = [x for x in open(os.path.join(g, "pytest_gpu.log")) if "passed" in x]
     out = [f"# {name} — {note}\n",
            "Command: `STAGES=\"smoke pytest bench ncu\" bash tools/gpu_round.sh`.  smoke ok; "
