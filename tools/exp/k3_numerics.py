@@ -112,7 +112,21 @@ def main():
         return y.reshape(-1) / np.sqrt(128.0)
 
     sk, sv = signs(11), signs(13)
-    if dither < 0:  # model check: everything exact
+    if os.environ.get("W13"):  # direction table dithered, rho applied in fp16 in-kernel
+        reps_n = dither_tables(dirs, dither or 16, rng)  # [R, K, K, 3]
+        rho16 = f16(rho_c)
+        pick_k = rng.integers(0, dither or 16, size=(T, 43))
+        pick_v = rng.integers(0, dither or 16, size=(T, 43))
+
+        reps_r = dither_tables(rho_c, dither or 16, rng)  # [R, KR]
+        if os.environ.get("W13") == "2":  # rho dithered too (per-lane register tables)
+            def tf(pick):
+                return lambda r, a, b: f16(reps_r[pick, r][..., None] * reps_n[pick, a, b])
+        else:
+            def tf(pick):
+                return lambda r, a, b: f16(rho16[r][..., None] * reps_n[pick, a, b])
+        kfn, vfn = tf(pick_k), tf(pick_v)
+    elif dither < 0:  # model check: everything exact
         kfn = vfn = lambda r, a, b: tab[r, a, b]
     elif dither:
         reps = dither_tables(tab, dither, rng)  # [R, KR, K, K, 3]

@@ -41,5 +41,27 @@ c2.append(torch.randn((B, Hkv, 128), device=dev), torch.randn((B, Hkv, 128), dev
 q = torch.randn((B, 7 * Hkv, 128), device=dev, generator=g)
 oq.attention_decode(q, cache)
 oq.attention_partials(q, cache, 0, cache.tokens)
+# 2-bit tiles: the 12-warp TMA-ring K3 (its default), with and without QJL keys,
+# and the 8-warp register variant
+for qjl in (False, True):
+    e2k = oq.Encoder(oq.CodecConfig(b_dir=3, b_nrm=1, qjl=qjl, rotation_seed=21))
+    e2v = oq.Encoder(oq.CodecConfig(b_dir=3, b_nrm=1, rotation_seed=22))
+    c3 = oq.KVCache(e2k, e2v, B, Hkv, 2000)
+    c3.pack(e2k.compress(torch.randn((B * Hkv * 2000, 128), device=dev, generator=g)),
+            e2v.compress(torch.randn((B * Hkv * 2000, 128), device=dev, generator=g)), 2000)
+    oq.attention_decode(q, c3)
+    oq.attention_decode(q, c3, n_splits=3)
+    oq.attention_partials(q, c3, 100, 1500)
+# the exact fp64 per-key API (exact_api.cu)
+for cfg in (oq.CodecConfig(b_dir=4, b_nrm=2), oq.CodecConfig(b_dir=5, b_nrm=3, qjl=True),
+            oq.CodecConfig(dim=64, b_dir=3, b_nrm=1)):
+    e = oq.Encoder(cfg)
+    r = e.compress(torch.randn((257, cfg.dim), device=dev, generator=g))
+    e.decode_exact(r)
+    e.reconstruct_rotated(r)
+    rot, sk = e.prepare(torch.randn((3, cfg.dim), device=dev, generator=g))
+    e.score_prepared(rot, sk, r)
+    e.attention_exact(torch.randn((2, cfg.dim), device=dev, generator=g), r,
+                      torch.randn((257, 16), device=dev, generator=g), n_splits=4)
 torch.cuda.synchronize()
 print("sanitize run ok")
