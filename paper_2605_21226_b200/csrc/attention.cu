@@ -393,7 +393,7 @@ struct WarpState {
   float m[2], l[2];
 };
 
-template <int W, bool QJL>
+template <int W, bool QJL, int PREV = 2>
 __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL>& R,
                                              const uint32_t (&qf)[Cfg<W, QJL>::QF],
                                              uint32_t toff, int tok0, int lo, int hi, int g,
@@ -479,7 +479,7 @@ __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL
 #ifndef OQ_PREV_QJL
 #define OQ_PREV_QJL 2
 #endif
-  constexpr int kPreV = QJL ? OQ_PREV_QJL : 2;  // V groups issued before the softmax
+  constexpr int kPreV = QJL ? OQ_PREV_QJL : PREV;  // V groups issued before the softmax
   uint2 e0[2][2][4];
 #pragma unroll
   for (int gg = 0; gg < kPreV; ++gg)
@@ -955,7 +955,11 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
         const size_t tn = tile + (size_t)RING * kAttnWarps;
         if (lane == 0 && tn < it.thi)
           ring_issue<W, QJL>(wr + st * C::STAGE, &s_ring_bar[warp][st], P, it.stream, tn);
-        process_tile<W, QJL>(S, r, qf, toff_of(tile), (int)(tile * kTileTok), it.lo, it.hi, g, c);
+#ifndef OQ_PREV_RING
+#define OQ_PREV_RING 2
+#endif
+        process_tile<W, QJL, OQ_PREV_RING>(S, r, qf, toff_of(tile), (int)(tile * kTileTok), it.lo,
+                                           it.hi, g, c);
         tile += kAttnWarps;
         st = st + 1 == RING ? 0 : st + 1;
       }

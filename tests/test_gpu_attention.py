@@ -68,21 +68,23 @@ def test_attention_matches_oracle(orc, cuda, b, qjl):
     assert e.max() <= TOL, (e.max(), e.mean())
 
 
+@pytest.mark.parametrize("b", [3, 2])
 @pytest.mark.parametrize("G", [1, 7, 8, 16])
-def test_gqa_group_sizes(orc, cuda, G):
+def test_gqa_group_sizes(orc, cuda, G, b):
     import torch
     B, Hkv, T = 1, 2, 257
     Hq = G * Hkv
-    d = build(orc, cuda, B, Hq, Hkv, T, seed=G)
+    d = build(orc, cuda, B, Hq, Hkv, T, b=b, seed=G)
     got = oq.attention_decode(torch.from_numpy(d["q"]).to(cuda), d["cache"]).cpu().numpy()
     assert rel_err(got, oracle_out(d, B, Hq, Hkv)).max() <= TOL
 
 
-def test_split_count_does_not_change_output(orc, cuda):
+@pytest.mark.parametrize("b,qjl", [(3, False), (2, False), (2, True)])
+def test_split_count_does_not_change_output(orc, cuda, b, qjl):
     # codec_test.cpp:301-319 at the batched level
     import torch
     B, Hq, Hkv, T = 2, 7, 1, 1000
-    d = build(orc, cuda, B, Hq, Hkv, T, seed=5)
+    d = build(orc, cuda, B, Hq, Hkv, T, b=b, qjl=qjl, seed=5)
     q = torch.from_numpy(d["q"]).to(cuda)
     outs = [oq.attention_decode(q, d["cache"], n_splits=s).cpu().numpy() for s in (1, 3, 8, 32)]
     # Different split counts change the running max each fp16 P operand is
@@ -92,19 +94,21 @@ def test_split_count_does_not_change_output(orc, cuda):
     assert rel_err(outs[0], oracle_out(d, B, Hq, Hkv)).max() <= TOL
 
 
-def test_single_key_returns_its_value_row(orc, cuda):
+@pytest.mark.parametrize("b,qjl", [(3, False), (2, False), (2, True)])
+def test_single_key_returns_its_value_row(orc, cuda, b, qjl):
     # codec_test.cpp:338-351: softmax over one key is exactly that value row
     import torch
-    d = build(orc, cuda, 1, 7, 1, 1, seed=6)
+    d = build(orc, cuda, 1, 7, 1, 1, b=b, qjl=qjl, seed=6)
     got = oq.attention_decode(torch.from_numpy(d["q"]).to(cuda), d["cache"]).cpu().numpy()
     for h in range(7):
         assert rel_err(got[0, h], d["vdec"][0, 0, 0]) <= 1e-3
 
 
-def test_ragged_lengths(orc, cuda):
+@pytest.mark.parametrize("b,qjl", [(3, False), (2, False), (2, True)])
+def test_ragged_lengths(orc, cuda, b, qjl):
     import torch
     B, Hq, Hkv, T = 3, 14, 2, 333
-    d = build(orc, cuda, B, Hq, Hkv, T, seed=7)
+    d = build(orc, cuda, B, Hq, Hkv, T, b=b, qjl=qjl, seed=7)
     lens = [333, 31, 0]
     sl = torch.tensor(lens, dtype=torch.int32, device=cuda)
     got = oq.attention_decode(torch.from_numpy(d["q"]).to(cuda), d["cache"],
@@ -114,7 +118,8 @@ def test_ragged_lengths(orc, cuda):
     assert np.all(got[2] == 0.0)
 
 
-def test_sharded_partials_merge_like_n_splits(orc, cuda):
+@pytest.mark.parametrize("b,qjl", [(3, False), (2, False), (2, True)])
+def test_sharded_partials_merge_like_n_splits(orc, cuda, b, qjl):
     """Sequence sharding: per-range partials merged in order == one pass.
 
     This is the single-GPU image of the multi-GPU mode (each range is what
@@ -122,7 +127,7 @@ def test_sharded_partials_merge_like_n_splits(orc, cuda):
     """
     import torch
     B, Hq, Hkv, T = 2, 14, 2, 1000
-    d = build(orc, cuda, B, Hq, Hkv, T, seed=8)
+    d = build(orc, cuda, B, Hq, Hkv, T, b=b, qjl=qjl, seed=8)
     q = torch.from_numpy(d["q"]).to(cuda)
     P = 4
     chunk = -(-T // P)
@@ -149,13 +154,14 @@ def test_rejects_bad_shapes(orc, cuda):
         oq.attention_decode(torch.from_numpy(d["q"]).to(cuda), d["cache"], T=41)
 
 
-def test_long_context_weighted_stream_k(orc, cuda):
+@pytest.mark.parametrize("b,qjl", [(3, False), (2, False), (2, True)])
+def test_long_context_weighted_stream_k(orc, cuda, b, qjl):
     """Contexts long enough for the weighted stream-K split (>= 512 tiles per
     stream: every stream start counts as extra tile units) against the
     reference, with ragged lengths and a partial token range."""
     import torch
     B, Hq, Hkv, T = 2, 14, 2, 20000
-    d = build(orc, cuda, B, Hq, Hkv, T, seed=9)
+    d = build(orc, cuda, B, Hq, Hkv, T, b=b, qjl=qjl, seed=9)
     q = torch.from_numpy(d["q"]).to(cuda)
     got = oq.attention_decode(q, d["cache"]).cpu().numpy()
     assert rel_err(got, oracle_out(d, B, Hq, Hkv)).max() <= TOL
@@ -172,12 +178,13 @@ def test_long_context_weighted_stream_k(orc, cuda):
     assert rel_err(out.reshape(B, Hq, 128).cpu().numpy(), full).max() <= TOL
 
 
-def test_attention_pipeline_host_buffers(orc, cuda):
+@pytest.mark.parametrize("b", [3, 2])
+def test_attention_pipeline_host_buffers(orc, cuda, b):
     """AttentionPipeline (host q in, host out back, copies on their own
     streams): every step's output equals attention_decode on the device."""
     import torch
     B, Hq, Hkv, T = 2, 14, 2, 3000
-    d = build(orc, cuda, B, Hq, Hkv, T, seed=11)
+    d = build(orc, cuda, B, Hq, Hkv, T, b=b, seed=11)
     pipe = oq.AttentionPipeline(d["cache"], Hq)
     g = torch.Generator().manual_seed(3)
     qs = [torch.randn((B, Hq, 128), generator=g).pin_memory() for _ in range(5)]

@@ -18,9 +18,9 @@ import paper_2605_21226_b200 as oq
 pytestmark = pytest.mark.gpu
 
 
-def _cache(cuda, B, Hkv, T):
+def _cache(cuda, B, Hkv, T, bits=3):
     import torch
-    bd, bn = oq.default_bit_split(3)
+    bd, bn = oq.default_bit_split(bits)
     ek = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=31))
     ev = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=32))
     g = torch.Generator(device=cuda).manual_seed(3)
@@ -32,9 +32,10 @@ def _cache(cuda, B, Hkv, T):
     return cache, q
 
 
-def test_single_rank_nccl_equals_decode(cuda):
+@pytest.mark.parametrize("bits", [3, 2])
+def test_single_rank_nccl_equals_decode(cuda, bits):
     B, Hkv, T = 2, 2, 3000
-    cache, q = _cache(cuda, B, Hkv, T)
+    cache, q = _cache(cuda, B, Hkv, T, bits)
     comm = oq.NcclComm(1, oq.NcclComm.unique_id(), 0)
     try:
         got = oq.attention_decode_sharded(q, cache, 0, T, comm)
@@ -45,11 +46,12 @@ def test_single_rank_nccl_equals_decode(cuda):
     assert err < 1e-5, err
 
 
+@pytest.mark.parametrize("bits", [3, 2])
 @pytest.mark.parametrize("P", [2, 3, 8])
-def test_rank_ordered_merge_matches_n_splits(cuda, P):
+def test_rank_ordered_merge_matches_n_splits(cuda, P, bits):
     import torch
     B, Hkv, T = 1, 2, 2500
-    cache, q = _cache(cuda, B, Hkv, T)
+    cache, q = _cache(cuda, B, Hkv, T, bits)
     rows = B * 7 * Hkv
     chunk = -(-T // P)
     parts = []
