@@ -38,8 +38,12 @@
 
 namespace oqd {
 
-constexpr int kCFWarps = 8;
-constexpr int kCFThreads = 32 * kCFWarps;
+#ifndef OQ_CF_NW5
+#define OQ_CF_NW5 8
+#endif
+#ifndef OQ_CF_DREP5
+#define OQ_CF_DREP5 2
+#endif
 constexpr int kCFRow = 132;  // floats per staged row (128 + 4 pad: conflict-free LDS.128)
 constexpr int kCFCells = 128, kCFLutRep = 8;  // LUT: float4 entries, 8 replicas
 
@@ -51,16 +55,19 @@ struct CFS {
   static constexpr int RB = QB + (QJL ? 18 : 0);        // record bytes
   static constexpr int RW = (RB + 3) / 4;               // record words
   // the QJL variants give up direction-table replicas for the larger records
-  static constexpr int DREP = QJL ? (BD <= 4 ? 4 : 1) : (BD <= 4 ? 8 : 2);
+  static constexpr int DREP = QJL ? (BD <= 4 ? 4 : 1) : (BD <= 4 ? 8 : OQ_CF_DREP5);
+  // warps per CTA (one CTA per SM): fewer at b_dir = 5 leave room for more
+  // direction-table replicas (bank conflicts of the 3x3 window lookups)
+  static constexpr int NW = (BD >= 5 && !QJL) ? OQ_CF_NW5 : 8;
   static constexpr int RECBUF_WORDS = (32 * RB) / 4 + 4;
   // shared memory carve (bytes)
   static constexpr int KP = K + 2;  // direction grid padded by a -inf border
   static constexpr int DIRS_BYTES = KP * KP * DREP * 16;
   static constexpr int LUT_BYTES = kCFCells * kCFLutRep * 16;
   static constexpr int BND_BYTES = 64 * 4;
-  static constexpr int ROWS_BYTES = kCFWarps * 32 * kCFRow * 4;
-  static constexpr int RECB_BYTES = kCFWarps * RECBUF_WORDS * 4;
-  static constexpr int SCR_BYTES = kCFWarps * 32 * (RW + 1) * 4;  // per-lane record words
+  static constexpr int ROWS_BYTES = NW * 32 * kCFRow * 4;
+  static constexpr int RECB_BYTES = NW * RECBUF_WORDS * 4;
+  static constexpr int SCR_BYTES = NW * 32 * (RW + 1) * 4;  // per-lane record words
   static constexpr int SMEM =
       DIRS_BYTES + LUT_BYTES + BND_BYTES + ROWS_BYTES + RECB_BYTES + SCR_BYTES + 64;
 };
@@ -87,7 +94,7 @@ __device__ __forceinline__ uint32_t cf_bucket(float x, float g, const float4* lu
 }
 
 template <int BD, int BN, int MODE, int DT, bool QJL>
-__global__ void __launch_bounds__(kCFThreads, 1)
+__global__ void __launch_bounds__(CFS<BD, BN, QJL>::NW * 32, 1)
     compress_fast_kernel(OqCodecParams p, const void* __restrict__ x, size_t n,
                          uint8_t* __restrict__ out, FlagEntry* __restrict__ flags,
                          uint32_t* __restrict__ flag_cnt) {
@@ -102,8 +109,8 @@ __global__ void __launch_bounds__(kCFThreads, 1)
   float* rows = reinterpret_cast<float*>(smem + S::DIRS_BYTES + S::LUT_BYTES + S::BND_BYTES);
   uint32_t* recb = reinterpret_cast<uint32_t*>(smem + S::DIRS_BYTES + S::LUT_BYTES +
                                                S::BND_BYTES + S::ROWS_BYTES);
-  uint32_t* scratch_all = recb + kCFWarps * S::RECBUF_WORDS;
-  __shared__ __align__(8) uint64_t bars[kCFWarps];
+  uint32_t* scratch_all = recb + S::NW * S::RECBUF_WORDS;
+  __shared__ __align__(8) uint64_t bars[S::NW];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // ---- tables -------------------------------------------------------------
@@ -118,12 +125,12 @@ __global__ void __launch_bounds__(kCFThreads, 1)
       v.w = 0.f;
     }
     return v;
-  }, tid, kCFThreads);
+  }, tid, S::NW * 32);
   if (tid <= K) bnd[tid] = tid == 0 ? -INFINITY : (tid == K ? INFINITY : (float)p.xi_bnd[tid - 1]);
   float* rho_s = bnd + 40;  // fp32 norm centroids (QJL residual)
   if (QJL && tid < S::KR) rho_s[tid] = p.rho32[tid];
   __syncthreads();
-  for (int c = tid; c < kCFCells; c += kCFThreads) {
+  for (int c = tid; c < kCFCells; c += S::NW * 32) {
     // guard band 1e-6 >> the fp32 error of the cell index
     const float x0 = -1.f + (float)c / (0.5f * kCFCells) - 1e-6f;
     const float x1 = -1.f + (float)(c + 1) / (0.5f * kCFCells) + 1e-6f;
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(kCFThreads, 1)
   __syncthreads();
 
   const size_t nblk = (n + 31) / 32;
-  const size_t wstride = (size_t)gridDim.x * kCFWarps;
+  const size_t wstride = (size_t)gridDim.x * S::NW;
   auto request = [&](size_t blk) {  // rows of block blk -> this warp's staging rows
     const size_t k0 = blk * 32;
     const int nk = (int)min((size_t)32, n - k0);
@@ -170,7 +177,7 @@ __global__ void __launch_bounds__(kCFThreads, 1)
           "r"(cf_smem(bar))
           : "memory");
   };
-  size_t blk = (size_t)blockIdx.x * kCFWarps + warp;
+  size_t blk = (size_t)blockIdx.x * S::NW + warp;
   if (blk < nblk) request(blk);
   uint32_t phase = 0;
   for (; blk < nblk; blk += wstride, phase ^= 1) {
@@ -538,10 +545,10 @@ static cudaError_t launch_cf_t(const OqCodecParams& p, const void* x, size_t n, 
   cudaError_t e = set_smem_once(compress_fast_kernel<BD, BN, MODE, DT, QJL>, S::SMEM);
   if (e != cudaSuccess) return e;
   const size_t nblk = (n + 31) / 32;
-  size_t grid = (nblk + kCFWarps - 1) / kCFWarps;
+  size_t grid = (nblk + S::NW - 1) / S::NW;
   if (grid > (size_t)num_sms) grid = num_sms;
   compress_fast_kernel<BD, BN, MODE, DT, QJL>
-      <<<(unsigned)grid, kCFThreads, S::SMEM, st>>>(p, x, n, out, flag_idx, flag_cnt);
+      <<<(unsigned)grid, S::NW * 32, S::SMEM, st>>>(p, x, n, out, flag_idx, flag_cnt);
   return cudaGetLastError();
 }
 

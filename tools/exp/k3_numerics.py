@@ -139,6 +139,8 @@ def main():
     else:
         kfn = vfn = lambda r, a, b: f16(tab[r, a, b])
     exact_fn = lambda r, a, b: tab[r, a, b]  # noqa: E731
+    if os.environ.get("KRN"):  # K side through a round-to-nearest table, V dithered
+        kfn = lambda r, a, b: f16(tab[r, a, b])  # noqa: E731
     gk, Kh = rows(kr, exact_fn if os.environ.get("KEXACT") else kfn)
     gv, Vh = rows(vr, exact_fn if os.environ.get("VEXACT") else vfn)
     out = np.zeros((7, 128))
