@@ -26,6 +26,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -1631,7 +1632,7 @@ cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecPara
   const int W = 2 * pk.b_dir + pk.b_nrm;
   // Warps per CTA (one CTA per SM) and the tile delivery: OQ_ATTN_WARPS /
   // OQ_ATTN_RING select a variant for tuning runs; the default is the
-  // measured best.  RING 0 = register ping-pong, 2 / 3 = TMA ring stages.
+  // measured best.  RING 0 = register ping-pong, 2 = two-stage TMA ring.
   static const int ring_env = [] {
     const char* e = getenv("OQ_ATTN_RING");
     return e ? atoi(e) : -1;
@@ -1640,24 +1641,32 @@ cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecPara
     const char* e = getenv("OQ_ATTN_WARPS");
     return e ? atoi(e) : -1;
   }();
-  // measured defaults (tools/exp/abn.sh, r02): the byte-coded 2-bit tiles
+  // measured defaults (tools/exp/abn.sh, r02; a 3-stage ring measured the
+  // same as 2 stages): the byte-coded 2-bit tiles
   // (W = 7, C4/C5) run 12 warps fed by a 2-stage TMA ring (C4 -10 %, C5
   // -1.7 %); the 10-bit tiles (C3) keep 8 warps with register prefetch (the
   // ring costs them 2-10 %)
   const int ring = ring_env >= 0 ? ring_env : (W == 7 ? 2 : 0);
   const int nw = nw_env > 0 ? nw_env : (ring ? 12 : 8);
-#define OQ_LAUNCH(WW, QQ)                                                                   \
-  if (W == WW && (bool)pk.qjl == QQ) {                                                     \
-    if (ring == 3 && nw == 12 && Cfg<WW, QQ>::smem(12, 3) <= kMaxSmem) return launch_attn_t<WW, QQ, 12, 3>(pk, a, splits, G, HC, st, num_sms); \
-    if (ring >= 2 && nw == 12 && Cfg<WW, QQ>::smem(12, 2) <= kMaxSmem) return launch_attn_t<WW, QQ, 12, 2>(pk, a, splits, G, HC, st, num_sms); \
-    if (ring >= 2 && Cfg<WW, QQ>::smem(8, 2) <= kMaxSmem) return launch_attn_t<WW, QQ, 8, 2>(pk, a, splits, G, HC, st, num_sms);  \
-    return launch_attn_t<WW, QQ, 8, 0>(pk, a, splits, G, HC, st, num_sms);                 \
-  }
-  OQ_LAUNCH(10, false)
-  OQ_LAUNCH(10, true)
-  OQ_LAUNCH(7, false)
-  OQ_LAUNCH(7, true)
-#undef OQ_LAUNCH
+  auto launch = [&](auto w_tag, auto q_tag) -> cudaError_t {
+    constexpr int WW = decltype(w_tag)::value;
+    constexpr bool QQ = decltype(q_tag)::value;
+    // only the variants that fit in shared memory are instantiated
+    if constexpr (Cfg<WW, QQ>::smem(12, 2) <= kMaxSmem)
+      if (ring >= 2 && nw == 12) return launch_attn_t<WW, QQ, 12, 2>(pk, a, splits, G, HC, st, num_sms);
+    if constexpr (Cfg<WW, QQ>::smem(8, 2) <= kMaxSmem)
+      if (ring >= 2) return launch_attn_t<WW, QQ, 8, 2>(pk, a, splits, G, HC, st, num_sms);
+    return launch_attn_t<WW, QQ, 8, 0>(pk, a, splits, G, HC, st, num_sms);
+  };
+  using I10 = std::integral_constant<int, 10>;
+  using I7 = std::integral_constant<int, 7>;
+  using T_ = std::true_type;
+  using F_ = std::false_type;
+  if (W == 10 && !pk.qjl) return launch(I10{}, F_{});
+  if (W == 10 && pk.qjl) return launch(I10{}, T_{});
+  if (W == 7 && !pk.qjl) return launch(I7{}, F_{});
+  if (W == 7 && pk.qjl) return launch(I7{}, T_{});
+
   (void)pv;
   return cudaErrorNotSupported;
 }
