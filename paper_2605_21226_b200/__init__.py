@@ -458,7 +458,7 @@ class KVCache:
         self.B, self.Hkv, self.cap = B, Hkv, int(cap_tokens)
         kt, vt = enc_k.tile_bytes(ROLE_K), enc_v.tile_bytes(ROLE_V)
         if kt == 0 or vt == 0:
-            raise NotImplementedError("attention tiles need dim 128 and 2*b_dir+b_nrm in {7,10}")
+            raise NotImplementedError("attention tiles need dim 128 and 2*b_dir+b_nrm in {7, 10, 13} (b = 2, 3, 4 at the default split)")
         ntiles = (self.cap + 31) // 32
         self.k = torch.zeros(B * Hkv * ntiles * kt, dtype=torch.uint8, device=device)
         self.v = torch.zeros(B * Hkv * ntiles * vt, dtype=torch.uint8, device=device)

@@ -60,6 +60,14 @@ __host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 // take one whole byte each, so one PRMT turns a code into its table address
 // (see code_addr); wider codes are packed back to back.
 __host__ __device__ constexpr int fw(int W) { return W <= 8 ? 8 : W; }
+// Dithered fp16 replicas of each joint-table entry in shared memory (see
+// stage_table_issue): 32 for byte-coded W <= 8, 16 for W = 10 (every
+// half-warp lookup conflict-free); W = 13 (b = 4, 8192 codes) fits only 2
+// (128 KB), so its lookups take bank conflicts.
+__host__ __device__ constexpr int table_rep(int W) { return W <= 8 ? 32 : W <= 10 ? 16 : 2; }
+__host__ __device__ constexpr int table_shift(int W) {  // log2(entry stride) = log2(8 * REP)
+  return W <= 8 ? 8 : W <= 10 ? 7 : 4;
+}
 __host__ __device__ inline int kw_full(int W) { return cdiv(44 * fw(W), 32); }
 __host__ __device__ inline int kw_3(int W) { return cdiv(40 * fw(W), 32); }
 __host__ __device__ inline int vw_full(int W) { return cdiv(48 * fw(W), 32); }
@@ -143,15 +151,21 @@ __device__ __forceinline__ uint32_t code_addr(const uint32_t (&w)[N], int slot, 
     const int i = slot >> 2, b = slot & 3;
     return __byte_perm(w[i], off, 0x7604 | (b << 4));
   }
+  constexpr int S = table_shift(W);  // entry stride 2^S bytes
   const int pos = slot * W, i = pos >> 5, sh = pos & 31;
   constexpr uint32_t M = (1u << W) - 1u;
   if (sh + W <= 32) {
     const uint32_t m = w[i] & (M << sh);  // LOP3
-    if (sh > 7) return mad_hi(m, 1u << (39 - sh), off);  // (m >> (sh - 7)) + off
-    return mad_lo(m, 1u << (7 - sh), off);               // (m << (7 - sh)) + off
+    if (sh > S) return mad_hi(m, 1u << (32 + S - sh), off);  // (m >> (sh - S)) + off
+    return mad_lo(m, 1u << (S - sh), off);                   // (m << (S - sh)) + off
   }
-  const uint32_t v = __funnelshift_r(w[i], w[i + 1], sh - 7);
-  return off + (v & (M << 7));
+  if (sh >= S) {
+    const uint32_t v = __funnelshift_r(w[i], w[i + 1], sh - S);
+    return off + (v & (M << S));
+  }
+  // (W = 13 only: a straddling field starting below bit S)
+  const uint32_t v = __funnelshift_r(w[i], w[i + 1], sh);
+  return off + ((v & M) << S);
 }
 
 // The dequant table in shared memory: NE codes x REP fp16 replicas of
@@ -280,7 +294,7 @@ struct Cfg {
   static constexpr int QF = 18 + (QJL ? 16 : 0);
   // W <= 8: the table lives at shared address 0x10000 (256-byte entries);
   // TAB_BYTES then spans from the start of dynamic smem to its end
-  static constexpr int TAB_BYTES = W <= 8 ? 0x10000 + (1 << W) * 256 : (1 << W) * 16 * 8;
+  static constexpr int TAB_BYTES = W <= 8 ? 0x10000 + (1 << W) * 256 : (1 << W) * table_rep(W) * 8;
   static constexpr int QS_FLOATS = 8 * 2 * 129;  // fused query prep scratch
   // per-warp region: the merge slot (8 heads x kPartW floats) and, with a
   // TMA ring of `ring` stages, the staged tiles (aliased: the ring is idle
@@ -865,7 +879,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ __align__(8) uint64_t s_tab_bar;
   uint32_t tbase;
-  constexpr uint32_t kRepMask = W <= 8 ? 31u : 15u;
+  constexpr uint32_t kRepMask = (uint32_t)table_rep(W) - 1u;
   if constexpr (W <= 8) {
     // table at shared address 0x10000: 32 replicas x 8 B per entry
     const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
@@ -873,7 +887,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
     stage_table_issue(smem + (0x10000u - base), P.tab, (1u << W) * 32u * 8u, &s_tab_bar, tid);
     tbase = 0x10000u;
   } else {
-    stage_table_issue(tab, P.tab, (1u << W) * 16u * 8u, &s_tab_bar, tid);
+    stage_table_issue(tab, P.tab, (1u << W) * (uint32_t)table_rep(W) * 8u, &s_tab_bar, tid);
     tbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1511,7 +1525,7 @@ size_t attention_qfrag_bytes(const OqCodecParams& pk) {
 bool attention_fast_path_ok(const OqCodecParams& pk, const OqCodecParams& pv) {
   const int W = 2 * pk.b_dir + pk.b_nrm;
   return pk.dim == 128 && pv.dim == 128 && pk.b_dir == pv.b_dir && pk.b_nrm == pv.b_nrm &&
-         (W == 7 || W == 10) && !pv.qjl;
+         (W == 7 || W == 10 || W == 13) && !pv.qjl;
 }
 
 cudaError_t launch_pack_tiles(const OqCodecParams& p, int role, const uint8_t* recs,
@@ -1645,9 +1659,10 @@ cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecPara
   // same as 2 stages): the byte-coded 2-bit tiles
   // (W = 7, C4/C5) run 12 warps fed by a 2-stage TMA ring (C4 -10 %, C5
   // -1.7 %); the 10-bit tiles (C3) keep 8 warps with register prefetch (the
-  // ring costs them 2-10 %)
-  const int ring = ring_env >= 0 ? ring_env : (W == 7 ? 2 : 0);
-  const int nw = nw_env > 0 ? nw_env : (ring ? 12 : 8);
+  // ring costs them 2-10 %); the 13-bit tiles (b = 4) need the ring's single
+  // register image (8 warps)
+  const int ring = ring_env >= 0 ? ring_env : (W == 10 ? 0 : 2);
+  const int nw = nw_env > 0 ? nw_env : (ring && W == 7 ? 12 : 8);
   auto launch = [&](auto w_tag, auto q_tag) -> cudaError_t {
     constexpr int WW = decltype(w_tag)::value;
     constexpr bool QQ = decltype(q_tag)::value;
@@ -1660,12 +1675,15 @@ cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecPara
   };
   using I10 = std::integral_constant<int, 10>;
   using I7 = std::integral_constant<int, 7>;
+  using I13 = std::integral_constant<int, 13>;
   using T_ = std::true_type;
   using F_ = std::false_type;
   if (W == 10 && !pk.qjl) return launch(I10{}, F_{});
   if (W == 10 && pk.qjl) return launch(I10{}, T_{});
   if (W == 7 && !pk.qjl) return launch(I7{}, F_{});
   if (W == 7 && pk.qjl) return launch(I7{}, T_{});
+  if (W == 13 && !pk.qjl) return launch(I13{}, F_{});
+  if (W == 13 && pk.qjl) return launch(I13{}, T_{});
 
   (void)pv;
   return cudaErrorNotSupported;

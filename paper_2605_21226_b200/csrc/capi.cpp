@@ -168,7 +168,8 @@ void f16_bracket(double x, uint16_t& lo, uint16_t& hi) {
 std::vector<uint2> joint_replicas(const std::vector<double>& dirs64, const std::vector<double>& rho_c,
                                   uint32_t b_dir, uint32_t b_nrm) {
   const uint32_t W = 2 * b_dir + b_nrm, K = 1u << b_dir;
-  const uint32_t REP = W <= 8 ? 32 : 16, LB = W <= 8 ? 5 : 4;
+  // replica count per entry: attention.cu table_rep()
+  const uint32_t REP = W <= 8 ? 32 : W <= 10 ? 16 : 2, LB = W <= 8 ? 5 : W <= 10 ? 4 : 1;
   std::vector<uint2> t(size_t(1) << W << LB);
   for (uint32_t code = 0; code < (1u << W); ++code) {
     const uint32_t a = code & (K - 1), b = (code >> b_dir) & (K - 1), r = code >> (2 * b_dir);

@@ -22,7 +22,7 @@ def _encoders(bits, qjl):
     return ek, ev
 
 
-@pytest.mark.parametrize("bits,qjl", [(3, False), (2, True), (2, False)])
+@pytest.mark.parametrize("bits,qjl", [(3, False), (2, True), (2, False), (4, False), (4, True)])
 def test_append_equals_pack(cuda, bits, qjl):
     import torch
     B, Hkv, T, cap = 2, 2, 70, 96

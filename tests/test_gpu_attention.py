@@ -57,7 +57,8 @@ def rel_err(got, ref):
     return num / np.maximum(den, 1e-30)
 
 
-@pytest.mark.parametrize("b,qjl", [(3, False), (2, False), (2, True), (3, True)])
+@pytest.mark.parametrize("b,qjl", [(3, False), (2, False), (2, True), (3, True), (4, False),
+                                   (4, True)])
 def test_attention_matches_oracle(orc, cuda, b, qjl):
     import torch
     B, Hq, Hkv, T = 2, 14, 2, 700
@@ -104,7 +105,7 @@ def test_single_key_returns_its_value_row(orc, cuda, b, qjl):
         assert rel_err(got[0, h], d["vdec"][0, 0, 0]) <= 1e-3
 
 
-@pytest.mark.parametrize("b,qjl", [(3, False), (2, False), (2, True)])
+@pytest.mark.parametrize("b,qjl", [(3, False), (2, False), (2, True), (4, True)])
 def test_ragged_lengths(orc, cuda, b, qjl):
     import torch
     B, Hq, Hkv, T = 3, 14, 2, 333
@@ -154,7 +155,7 @@ def test_rejects_bad_shapes(orc, cuda):
         oq.attention_decode(torch.from_numpy(d["q"]).to(cuda), d["cache"], T=41)
 
 
-@pytest.mark.parametrize("b,qjl", [(3, False), (2, False), (2, True)])
+@pytest.mark.parametrize("b,qjl", [(3, False), (2, False), (2, True), (4, False)])
 def test_long_context_weighted_stream_k(orc, cuda, b, qjl):
     """Contexts long enough for the weighted stream-K split (>= 512 tiles per
     stream: every stream start counts as extra tile units) against the

@@ -250,3 +250,16 @@ def test_large_value_norms(orc, cuda, bits, qjl):
     got = oq.attention_decode(q.to(cuda), cache).cpu().numpy()
     assert np.all(np.isfinite(got))
     compare(got, oracle_rows(ok, ov, host, q.numpy(), Hkv, Hq // Hkv))
+
+
+def test_b4_tiles_long_context(orc, cuda):
+    """b = 4 (W = 13) tiles at a 64K-token context: the joint table fits only
+    two dithered replicas in shared memory (attention.cu table_rep), so this
+    is where its residual fp16 bias would show."""
+    import torch
+    B, Hq, Hkv, T = 1, 14, 2, 65536
+    cache, host, ok, ov = build_bench_cache(orc, cuda, 4, False, B, Hkv, T, [0, 1], seed=4)
+    check_codes(ok, ov, host, n_check=1 << 14)
+    q = torch.randn((B, Hq, 128), generator=torch.Generator().manual_seed(95))
+    got = oq.attention_decode(q.to(cuda), cache).cpu().numpy()
+    compare(got, oracle_rows(ok, ov, host, q.numpy(), Hkv, Hq // Hkv))

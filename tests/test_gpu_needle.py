@@ -12,9 +12,9 @@ octo_qjl b=3/4 within 0.01 of fp32 (means over 128 seeds).
 Here the keys are compressed by K1 on the GPU and the mass is read out of the
 GPU attention: V holds one Gaussian row for the needle and zero rows for the
 distractors (a zero vector encodes to gamma = 0 and decodes exactly to 0), so
-out = p_0 * v_hat_0 and mass = out . v_hat_0 / |v_hat_0|^2.  b = 2 (W = 7)
-and b = 3 + QJL (W = 10) run the compressed-V tile kernel (K3); b = 4 + QJL
-runs the general path with dense values (values = e_0, vdim = 1).  Each
+out = p_0 * v_hat_0 and mass = out . v_hat_0 / |v_hat_0|^2.  All three run
+the compressed-V tile kernel (K3): b = 2 (W = 7), b = 3 + QJL (W = 10), b = 4
++ QJL (W = 13).  Each
 seed's GPU mass is also compared with the mass computed from the oracle's
 fp64 Encoder::score on the same codes.
 """
@@ -36,7 +36,7 @@ def gpu_mass(orc, cuda, seed, bits, qjl):
     kr = ek.compress(torch.from_numpy(keys).to(cuda))  # fp64 keys, as the harness feeds them
     n = keys.shape[0]
     # attention_decode scales by 1/sqrt(dim): softmax(score / sqrt(d)) == run_needle's logits
-    if ek.tile_bytes(0) and not (bits == 4):
+    if ek.tile_bytes(0):
         ev = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=(rot + 1) & 0xFFFFFFFFFFFFFFFF))
         v = torch.zeros((n, D), dtype=torch.float64, device=cuda)
         v[0] = torch.from_numpy(_gauss(orc, orc.L.orc_stream_child(rot, 9), D)).to(cuda)
