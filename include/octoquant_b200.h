@@ -184,6 +184,8 @@ oq_status oq_cache_append_kv(const oq_codec* ck, const oq_codec* cv, const void*
                              int dtype, uint64_t n_streams, const int64_t* pos_dev, int64_t pos,
                              void* k_records, void* v_records, void* ktiles, void* vtiles,
                              uint64_t cap_tokens, void* stream);
+/* Tile formats exist for dim = 128 and 2*b_dir + b_nrm in {7, 10, 13} (b = 2,
+ * 3, 4 at the default split); 0 otherwise (use oq_attention_decode_dense). */
 size_t oq_cache_tile_bytes(const oq_codec* codec, int role); /* bytes per 32-token tile */
 size_t oq_cache_bytes(const oq_codec* codec, int role, uint64_t tokens); /* per stream */
 /* records: device [n_streams][rec_stride_tokens] records of n_tokens each

@@ -1501,7 +1501,8 @@ cudaError_t launch_append_token(const OqCodecParams& p, int role, const uint8_t*
 // ---------------------------------------------------------------------------
 size_t attention_tile_bytes(const OqCodecParams& p, int role) {
   const int W = 2 * p.b_dir + p.b_nrm;
-  if (p.dim != 128 || W > 13 || W < 3) return 0;
+  // the attention kernels exist for W = 7, 10, 13 (b = 2, 3, 4 at the default split)
+  if (p.dim != 128 || (W != 7 && W != 10 && W != 13)) return 0;
   return role == 0 ? ktile_bytes(W, p.qjl) : vtile_bytes(W);
 }
 
