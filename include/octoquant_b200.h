@@ -240,6 +240,33 @@ oq_status oq_attention_decode_sharded(const oq_codec* ck, const oq_codec* cv,
                                       uint64_t t_end, void* nccl_comm, int nranks, float* out,
                                       int n_splits, void* workspace, size_t ws_bytes,
                                       void* stream);
+/* ---- the same sequence sharding fused into the attention kernel over peer
+ * memory (no collective library) -------------------------------------------
+ * Each rank owns an exchange buffer of oq_attention_p2p_exchange_bytes bytes,
+ * zeroed once, from oq_device_alloc; xbufs[r] is rank r's buffer as mapped in
+ * THIS process (its own pointer for r == rank, oq_ipc_open of rank r's
+ * oq_ipc_handle otherwise).  In ONE launch the CTA that finalises a (b, kv
+ * head) stream writes this rank's merged (m, l, acc) rows into slot `rank` of
+ * every rank's buffer over NVLink, releases a flag there (= epoch), waits for
+ * every rank's flag in its own buffer and merges the ranks in rank order —
+ * the chunk merge of attention_decode(..., n_splits = nranks)
+ * (attention.hpp:60-69) — into out [B, Hq, dim], identical on all ranks.
+ * epoch: nonzero, strictly increasing per call (flags are never reset).
+ * Every rank must make the call (as with a collective); a missing rank makes
+ * the kernel trap after 20 s.  max_ctas: 0 = one CTA per SM (tests running
+ * several ranks on one GPU pass SMs / nranks so all ranks are resident).
+ * workspace: oq_attention_workspace_bytes(ck, cv, shape, 0), zero-filled. */
+size_t oq_attention_p2p_exchange_bytes(const oq_codec* ck, const oq_attn_shape* shape,
+                                       int nranks);
+oq_status oq_attention_decode_p2p(const oq_codec* ck, const oq_codec* cv,
+                                  const oq_attn_shape* shape, const float* q, const void* kcache,
+                                  const void* vcache, uint64_t t_begin, uint64_t t_end, int rank,
+                                  int nranks, void* const* xbufs, uint32_t epoch, int max_ctas,
+                                  float* out, void* workspace, size_t ws_bytes, void* stream);
+/* CUDA IPC of device buffers between the ranks' processes (64-byte handles). */
+oq_status oq_ipc_handle(void* dev_ptr, uint8_t handle[64]);
+oq_status oq_ipc_open(const uint8_t handle[64], void** dev_ptr);
+oq_status oq_ipc_close(void* dev_ptr);
 /* NCCL helpers for callers without their own NCCL setup (tests, the C++
  * header): unique id (128 bytes) on one rank, broadcast it, then init. */
 oq_status oq_nccl_get_unique_id(uint8_t id[128]);

@@ -279,6 +279,13 @@ struct AttnKParams {
   const float* q;        // [B, Hq, 128]
   float* out;            // [B * Hq, 128] (or [B * Hq, kPartW] with out_partial)
   uint32_t* counters;    // [n_sh], zero on entry and exit
+  // P2P sequence sharding (oq_attention_decode_p2p): the CTA that finalises a
+  // stream writes this rank's merged rows into slot `rank` of every rank's
+  // exchange buffer over peer memory, raises its flag there, waits for all
+  // ranks' flags in its own buffer and merges the ranks in order into out
+  int p2p_nranks, p2p_rank;
+  uint32_t p2p_epoch;
+  uint8_t* p2p_xbuf[8];  // rank r's exchange buffer, mapped in this process
   uint32_t smask[4], qmask[4], vmask[4];
   float inv_sqrt_d;
 };
@@ -797,11 +804,12 @@ __device__ __forceinline__ void seg_qprep(uint32_t (&qf)[QF], const AttnKParams&
 // combine_kernel's finalize = 0, for a later cross-rank merge) instead.
 __device__ __forceinline__ void combine_row(const float* base, int n, float* out,
                                             const uint32_t (&vmask)[4], float inv_sqrt_d,
-                                            int lane, bool partial = false) {
+                                            int lane, bool partial = false,
+                                            size_t stride = kPartW) {
   const float NEG_INF = -__int_as_float(0x7f800000);
   float M = NEG_INF;
   for (int i = lane; i < n; i += 32) {
-    const float2 ml = *reinterpret_cast<const float2*>(base + (size_t)i * kPartW);
+    const float2 ml = *reinterpret_cast<const float2*>(base + (size_t)i * stride);
     if (ml.y > 0.f) M = fmaxf(M, ml.x);
   }
 #pragma unroll
@@ -816,8 +824,8 @@ __device__ __forceinline__ void combine_row(const float* base, int n, float* out
 #pragma unroll
     for (int j = 0; j < NB; ++j) {  // past the end: re-read the last part, skipped below
       const size_t i = (size_t)min(i0 + j, n - 1);
-      ml[j] = *reinterpret_cast<const float2*>(base + i * kPartW);
-      a4[j] = *reinterpret_cast<const float4*>(base + i * kPartW + 4 + 4 * lane);
+      ml[j] = *reinterpret_cast<const float2*>(base + i * stride);
+      a4[j] = *reinterpret_cast<const float4*>(base + i * stride + 4 + 4 * lane);
     }
 #pragma unroll
     for (int j = 0; j < NB; ++j)
@@ -844,6 +852,70 @@ __device__ __forceinline__ void combine_row(const float* base, int n, float* out
     r[i] = ((vmask[e >> 5] >> (e & 31)) & 1u) ? -v : v;
   }
   *reinterpret_cast<float4*>(out + 4 * lane) = make_float4(r[0], r[1], r[2], r[3]);
+}
+
+// Fused P2P sequence sharding, run by the CTA that finalises stream chunk
+// `it` on this rank (all its threads):
+//  (1) this rank's merged rows of the chunk -> shared staging;
+//  (2) stored into slot `rank` of EVERY rank's exchange buffer — peer memory
+//      over NVLink, mapped into this process (CUDA IPC);
+//  (3) a system-scope release of flag [rank][chunk] = epoch in each buffer;
+//  (4) an acquire-spin on this buffer's flags [r][chunk] for every rank r;
+//  (5) the ranks' rows merged in rank order — attention_decode(...,
+//      n_splits = nranks), attention.hpp:60-69 — and finalised into out.
+// One launch per step, no collective library; every rank ends with the same
+// rows.  A rank that never arrives traps after 20 s instead of hanging.
+// Exchange buffer layout: float [2][nranks][B*Hq][kPartW] (the half is the
+// epoch's parity: a rank can start the next call while a slower one still
+// reads this call's rows), then u32 flags [nranks][n_sh] (zeroed once; epochs
+// increase per call, and a flag that has already moved on counts as arrived).
+__device__ __noinline__ void p2p_exchange(const AttnKParams& P, const Seg& it, int nparts,
+                                          float* stage, int tid, int warp, int lane, int nwarps) {
+  const int nh = min(8, P.G - 8 * it.hc);
+  const size_t rows_total = (size_t)P.B * P.Hq;
+  const size_t row0 = (size_t)it.b * P.Hq + (size_t)it.kvh * P.G + 8 * it.hc;
+  for (int w = warp; w < nh; w += nwarps)
+    combine_row(P.partials + (row0 + w) * P.n_parts * kPartW, nparts, stage + w * kPartW,
+                P.vmask, P.inv_sqrt_d, lane, true);
+  __syncthreads();
+  const size_t half = (size_t)(P.p2p_epoch & 1u) * P.p2p_nranks * rows_total * kPartW;
+  for (int r = 0; r < P.p2p_nranks; ++r) {
+    float* dst = reinterpret_cast<float*>(P.p2p_xbuf[r]) + half +
+                 ((size_t)P.p2p_rank * rows_total + row0) * kPartW;
+    for (int i = tid; i < nh * kPartW / 4; i += blockDim.x)
+      reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(stage)[i];
+  }
+  __syncthreads();
+  const size_t flag_off = 2 * (size_t)P.p2p_nranks * rows_total * kPartW * sizeof(float);
+  if (tid == 0) {
+    __threadfence_system();
+    for (int r = 0; r < P.p2p_nranks; ++r) {
+      uint32_t* fl = reinterpret_cast<uint32_t*>(P.p2p_xbuf[r] + flag_off) +
+                     (size_t)P.p2p_rank * P.n_sh + it.sh;
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(fl), "r"(P.p2p_epoch) : "memory");
+    }
+    const uint32_t* mine = reinterpret_cast<const uint32_t*>(P.p2p_xbuf[P.p2p_rank] + flag_off);
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int r = 0; r < P.p2p_nranks; ++r) {
+      for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];"
+                     : "=r"(v)
+                     : "l"(mine + (size_t)r * P.n_sh + it.sh)
+                     : "memory");
+        if ((int32_t)(v - P.p2p_epoch) >= 0) break;
+        uint64_t now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (now - t0 > 20000000000ull) __trap();
+      }
+    }
+  }
+  __syncthreads();
+  const float* xl = reinterpret_cast<const float*>(P.p2p_xbuf[P.p2p_rank]) + half;
+  for (int w = warp; w < nh; w += nwarps)
+    combine_row(xl + (row0 + w) * kPartW, P.p2p_nranks, P.out + (row0 + w) * 128, P.vmask,
+                P.inv_sqrt_d, lane, false, rows_total * kPartW);
 }
 
 // Variant A: each warp streams its tiles from HBM straight into registers,
@@ -1018,7 +1090,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
         if (s_last) P.counters[it.sh] = 0u;
       }
       __syncthreads();
-      if (s_last) {
+      if (s_last && P.p2p_nranks > 0) {
+        p2p_exchange(P, it, nparts, qs, tid, warp, lane, kAttnWarps);
+      } else if (s_last) {
         for (int w = warp; w < 8; w += kAttnWarps) {
           if (8 * it.hc + w >= P.G) continue;
           const size_t row = (size_t)it.b * P.Hq + (size_t)it.kvh * P.G + 8 * it.hc + w;
@@ -1574,6 +1648,10 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
   }
   P.fuse = a.out != nullptr && a.counters != nullptr;
   P.out_partial = a.out_partial;
+  P.p2p_nranks = a.p2p_nranks;
+  P.p2p_rank = a.p2p_rank;
+  P.p2p_epoch = a.p2p_epoch;
+  for (int i = 0; i < 8; ++i) P.p2p_xbuf[i] = i < a.p2p_nranks ? a.p2p_xbuf[i] : nullptr;
   P.qjl = pk.qjl;
   P.q = a.q;
   P.out = a.out;
@@ -1594,6 +1672,7 @@ static cudaError_t launch_attn_t(const OqCodecParams& pk, const AttnArgs& a, int
     // 32 at 1024)
     P.sko = sko_env >= 0 ? (size_t)sko_env : (P.tps >= 2048 ? 48 : P.tps >= 512 ? 32 : 0);
   }
+  if (a.max_ctas > 0 && a.max_ctas < num_sms) num_sms = a.max_ctas;
   int grid = P.n_items < num_sms ? P.n_items : num_sms;
   if (P.streamk) {
     const size_t U = (size_t)P.n_sh * P.tps;

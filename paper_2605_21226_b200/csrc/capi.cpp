@@ -688,11 +688,18 @@ static oq_status attn_check(const oq_codec* ck, const oq_codec* cv, const oq_att
   return OQ_OK;
 }
 
+struct P2PArgs {
+  int rank, nranks;
+  uint32_t epoch;
+  uint8_t* xbuf[8];
+  int max_ctas;
+};
+
 static oq_status run_partials(const oq_codec* ck, const oq_codec* cv, const oq_attn_shape* sh,
                               const float* q, const void* kc, const void* vc, uint64_t t0,
                               uint64_t t1, int n_splits, void* ws, cudaStream_t st,
                               float** parts_out, int* n_parts_out, float* fused_out = nullptr,
-                              bool fused_partial = false) {
+                              bool fused_partial = false, const P2PArgs* p2p = nullptr) {
   const size_t rows = (size_t)sh->B * sh->Hq;
   const int np_max = parts_per_row(ck, sh, 0, sh->T, n_splits) + 1;
   const int np = parts_per_row(ck, sh, t0, t1, n_splits);
@@ -728,11 +735,19 @@ static oq_status run_partials(const oq_codec* ck, const oq_codec* cv, const oq_a
   const size_t n_sh = (size_t)sh->B * sh->Hkv * ((sh->Hq / sh->Hkv + 7) / 8);
   const bool fuse = fused_out && n_sh * 4 <= kCounterBytes && !getenv("OQ_ATTN_UNFUSED");
   cudaError_t e = cudaSuccess;
+  if (p2p && !fuse) return fail(OQ_ERR_UNSUPPORTED, "P2P sharding needs the fused attention kernel");
   if (fuse) {
     a.out = fused_out;
     a.out_partial = fused_partial ? 1 : 0;
     a.counters = reinterpret_cast<uint32_t*>(w8);
     for (int i = 0; i < 4; ++i) a.vmask[i] = cv->p.sign_mask[i];
+    if (p2p) {
+      a.p2p_nranks = p2p->nranks;
+      a.p2p_rank = p2p->rank;
+      a.p2p_epoch = p2p->epoch;
+      for (int i = 0; i < p2p->nranks; ++i) a.p2p_xbuf[i] = p2p->xbuf[i];
+      a.max_ctas = p2p->max_ctas;
+    }
   } else {
     e = oqd::launch_qprep(ck->p, a, st);
     if (e != cudaSuccess) return cuda_fail(e, "qprep kernel");
@@ -893,6 +908,65 @@ oq_status oq_attention_decode_sharded(const oq_codec* ck, const oq_codec* cv,
     return nccl_fail(r, "ncclAllGather");
   e = oqd::launch_attention_combine(cv->p, gather, rows, nranks, w, per, 1, out, st);
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "combine kernel");
+}
+
+// ---- fused P2P sequence sharding (peer memory, no collective library) -----
+size_t oq_attention_p2p_exchange_bytes(const oq_codec* ck, const oq_attn_shape* sh, int nranks) {
+  if (!ck || !sh || nranks < 1) return 0;
+  const size_t rows = (size_t)sh->B * sh->Hq;
+  const size_t n_sh = (size_t)sh->B * sh->Hkv * ((sh->Hq / (sh->Hkv ? sh->Hkv : 1) + 7) / 8);
+  return 2 * (size_t)nranks * rows * (4 + ck->cfg.dim) * sizeof(float) + (size_t)nranks * n_sh * 4;
+}
+
+oq_status oq_attention_decode_p2p(const oq_codec* ck, const oq_codec* cv, const oq_attn_shape* sh,
+                                  const float* q, const void* kc, const void* vc, uint64_t t0,
+                                  uint64_t t1, int rank, int nranks, void* const* xbufs,
+                                  uint32_t epoch, int max_ctas, float* out, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  const size_t base = oq_attention_workspace_bytes(ck, cv, sh, 0);
+  oq_status s = attn_check(ck, cv, sh, q, kc, vc, 0, base);
+  if (s) return s;
+  if (!out || !ws || !xbufs) return fail(OQ_ERR_INVALID_ARGUMENT, "null argument");
+  if (nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks)
+    return fail(OQ_ERR_INVALID_ARGUMENT, "P2P sharding supports 1..8 ranks");
+  if (epoch == 0) return fail(OQ_ERR_INVALID_ARGUMENT, "epoch must be nonzero (flags start at 0)");
+  if (t0 > t1 || t1 > sh->T) return fail(OQ_ERR_INVALID_ARGUMENT, "bad token range");
+  if (ws_bytes < base) return fail(OQ_ERR_INVALID_ARGUMENT, "workspace too small");
+  if (ck->cfg.dim != 128) return fail(OQ_ERR_UNSUPPORTED, "P2P sharding needs dim 128");
+  P2PArgs p{rank, nranks, epoch, {}, max_ctas};
+  for (int r = 0; r < nranks; ++r) {
+    if (!xbufs[r]) return fail(OQ_ERR_INVALID_ARGUMENT, "null exchange buffer");
+    p.xbuf[r] = static_cast<uint8_t*>(xbufs[r]);
+  }
+  float* parts = nullptr;
+  int np = 0;
+  // an empty token range still has to publish (empty) rows and wait: not
+  // representable by the memset shortcut, so it is rejected
+  if (t1 <= t0) return fail(OQ_ERR_UNSUPPORTED, "P2P sharding needs a nonempty token range per rank");
+  return run_partials(ck, cv, sh, q, kc, vc, t0, t1, 0, ws, as_stream(stream), &parts, &np, out,
+                      false, &p);
+}
+
+oq_status oq_ipc_handle(void* dev_ptr, uint8_t handle[64]) {
+  if (!dev_ptr || !handle) return fail(OQ_ERR_INVALID_ARGUMENT, "null argument");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, dev_ptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  std::memcpy(handle, &h, 64);
+  return OQ_OK;
+}
+
+oq_status oq_ipc_open(const uint8_t handle[64], void** dev_ptr) {
+  if (!dev_ptr || !handle) return fail(OQ_ERR_INVALID_ARGUMENT, "null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "cudaIpcOpenMemHandle");
+}
+
+oq_status oq_ipc_close(void* dev_ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
 }
 
 oq_status oq_nccl_get_unique_id(uint8_t id[128]) {

@@ -75,6 +75,11 @@ struct AttnArgs {
   uint32_t* counters = nullptr;  // [B*Hkv*ceil(G/8)] zero on entry, left zero
   int out_partial = 0;  // fused: out rows are merged (m, l, 0, 0, acc[D]) partials
   uint32_t vmask[4] = {0, 0, 0, 0};  // V rotation signs (for the fused combine)
+  // fused P2P sequence sharding (oq_attention_decode_p2p); p2p_nranks = 0: off
+  int p2p_nranks = 0, p2p_rank = 0;
+  uint32_t p2p_epoch = 0;
+  uint8_t* p2p_xbuf[8] = {};
+  int max_ctas = 0;  // 0: one CTA per SM
 };
 
 size_t attention_tile_bytes(const OqCodecParams& p, int role);  // role 0 = K, 1 = V
