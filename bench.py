@@ -444,10 +444,13 @@ def main():
 
     # the sharded step through the library's own NCCL path (fused K3 writes
     # this rank's partial into the gather buffer, ncclAllGather, merge: one
-    # C call) or through torch.distributed (OQ_BENCH_NCCL=torch)
-    native = sharded and os.environ.get("OQ_BENCH_NCCL", "native") == "native"
+    # C call), through torch.distributed (OQ_BENCH_NCCL=torch), or fused over
+    # peer memory in ONE launch (OQ_BENCH_P2P=1: P2PExchange, CUDA IPC)
+    p2p = sharded and os.environ.get("OQ_BENCH_P2P") == "1"
+    native = sharded and not p2p and os.environ.get("OQ_BENCH_NCCL", "native") == "native"
     comm = None
     nccl_info = None
+    xchg = oq.P2PExchange(cache, Hq) if p2p else None
     if native:
         uid = [oq.NcclComm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -459,9 +462,14 @@ def main():
         nccl_info = {"rank": r_nccl, "nranks": n_nccl, "source": "ncclCommUserRank/ncclCommCount"}
 
     def make_step(cache_, out_, gathered_, rows_):
+        xc = xchg if cache_ is cache else (oq.P2PExchange(cache_, Hq)
+                                            if p2p else None)
+
         def step(qd):
             if not sharded:
                 return oq.attention_decode(qd, cache_, n_splits=splits, out=out_)
+            if p2p:
+                return xc.decode(qd, cache_, 0, cache_.tokens, out=out_)
             if native:
                 return oq.attention_decode_sharded(qd, cache_, 0, cache_.tokens, comm,
                                                    n_splits=splits, out=out_)
@@ -704,7 +712,9 @@ def main():
             "clocks": clk.summary(),
             # world 1: one fused K3 launch per step; sharded: the fused K3
             # (writing this rank's partial) + the merge after the NCCL all-gather
-            "gpu_launches": (2 if sharded else 1) * args.steps,
+            "gpu_launches": (2 if sharded and not p2p else 1) * args.steps,
+            "sharded_exchange": (None if not sharded else "p2p: peer stores + flags inside K3 (CUDA IPC)"
+                                 if p2p else "ncclAllGather" if native else "torch.distributed"),
             "nccl": nccl_info,
             "b1": b1,
             "compress": comp,
@@ -716,6 +726,8 @@ def main():
         dist.barrier()
         if comm is not None:
             comm.close()
+        if xchg is not None:
+            xchg.close()
         dist.destroy_process_group()
     return 0
 

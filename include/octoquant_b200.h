@@ -292,6 +292,7 @@ oq_status oq_attention_decode_dense(const oq_codec* codec, const float* q, int n
 /* ---- device memory helpers (so C/C++ callers need no CUDA headers) ------- */
 oq_status oq_device_alloc(size_t bytes, void** ptr);
 oq_status oq_device_free(void* ptr);
+oq_status oq_device_memset(void* ptr, int value, size_t bytes);  /* synchronizes */
 oq_status oq_copy_to_device(void* dst, const void* src, size_t bytes);
 oq_status oq_copy_to_host(void* dst, const void* src, size_t bytes);  /* synchronizes */
 

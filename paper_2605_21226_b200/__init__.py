@@ -102,6 +102,15 @@ def lib():
         "oq_nccl_comm_init_rank": ([C.POINTER(vp), i32, vp, i32], i32),
         "oq_nccl_comm_destroy": ([vp], i32),
         "oq_nccl_comm_info": ([vp, C.POINTER(i32), C.POINTER(i32)], i32),
+        "oq_attention_p2p_exchange_bytes": ([vp, C.POINTER(_Shape), i32], sz),
+        "oq_attention_decode_p2p": ([vp, vp, C.POINTER(_Shape), vp, vp, vp, u64, u64, i32, i32,
+                                     C.POINTER(vp), C.c_uint32, i32, vp, vp, sz, vp], i32),
+        "oq_ipc_handle": ([vp, vp], i32),
+        "oq_ipc_open": ([vp, C.POINTER(vp)], i32),
+        "oq_ipc_close": ([vp], i32),
+        "oq_device_alloc": ([sz, C.POINTER(vp)], i32),
+        "oq_device_free": ([vp], i32),
+        "oq_device_memset": ([vp, i32, sz], i32),
         "oq_cache_append": ([vp, i32, vp, i32, C.c_uint64, vp, C.c_int64, vp, vp, C.c_uint64, vp],
                             i32),
         "oq_cache_append_kv": ([vp, vp, vp, vp, i32, C.c_uint64, vp, C.c_int64, vp, vp, vp, vp,
@@ -794,6 +803,88 @@ def attention_decode_sharded(q, cache: KVCache, t_begin, t_end, comm: NcclComm, 
                                              n_splits, _ptr(ws), ws.numel(),
                                              C.c_void_p(st.cuda_stream)))
     return out
+
+
+def p2p_exchange_bytes(cache: KVCache, Hq, nranks):
+    """Bytes of one rank's exchange buffer for attention_decode_p2p."""
+    sh = _shape(cache, Hq, cache.cap, None)
+    return lib().oq_attention_p2p_exchange_bytes(cache.enc_k.handle, C.byref(sh), nranks)
+
+
+def attention_decode_p2p(q, cache: KVCache, t_begin, t_end, rank, nranks, xbufs, epoch, T=None,
+                         out=None, max_ctas=0, stream=None):
+    """Sequence-sharded attention_decode fused over peer memory (one launch, no
+    collective library): this rank's tokens [t_begin, t_end) of ``cache``;
+    ``xbufs`` = the nranks exchange buffers (device pointers as mapped in this
+    process, or CUDA tensors); ``epoch`` nonzero and increasing per call.
+    Every rank gets the same [B, Hq, dim] output (oq_attention_decode_p2p)."""
+    import torch
+    _check_query(q, cache)
+    B, Hq, D = q.shape
+    T = cache.tokens if T is None else T
+    sh = _shape(cache, Hq, T, None)
+    L = lib()
+    ws_bytes = L.oq_attention_workspace_bytes(cache.enc_k.handle, cache.enc_v.handle,
+                                              C.byref(sh), 0)
+    st = _launch_stream(stream, q.device)
+    ptrs = (C.c_void_p * nranks)(*[C.c_void_p(x.data_ptr() if hasattr(x, "data_ptr") else int(x))
+                                   for x in xbufs])
+    with torch.cuda.stream(st):
+        ws = _Workspace.get(ws_bytes, q.device, st)
+        if out is None:
+            out = torch.empty((B, Hq, D), dtype=torch.float32, device=q.device)
+        q = q.contiguous().float()
+        _check(L.oq_attention_decode_p2p(cache.enc_k.handle, cache.enc_v.handle, C.byref(sh),
+                                         _ptr(q), _ptr(cache.k), _ptr(cache.v), t_begin, t_end,
+                                         rank, nranks, ptrs, epoch, max_ctas, _ptr(out), _ptr(ws),
+                                         ws.numel(), C.c_void_p(st.cuda_stream)))
+    return out
+
+
+class P2PExchange:
+    """The exchange buffers of attention_decode_p2p across one process per GPU:
+    this rank's buffer comes from cudaMalloc (zero-filled), its CUDA IPC handle
+    is shared through torch.distributed (``group``), and the peers' buffers are
+    mapped into this process.  ``decode`` is then one fused launch per step."""
+
+    def __init__(self, cache: KVCache, Hq, group=None):
+        import torch.distributed as dist
+        self.rank, self.nranks = dist.get_rank(group), dist.get_world_size(group)
+        L = lib()
+        nbytes = p2p_exchange_bytes(cache, Hq, self.nranks)
+        own = C.c_void_p()
+        _check(L.oq_device_alloc(nbytes, C.byref(own)))
+        _check(L.oq_device_memset(own, 0, nbytes))
+        self._own = own
+        h = (C.c_uint8 * 64)()
+        _check(L.oq_ipc_handle(own, h))
+        handles = [None] * self.nranks
+        dist.all_gather_object(handles, bytes(h), group=group)
+        self.ptrs, self._opened = [], []
+        for r, hb in enumerate(handles):
+            if r == self.rank:
+                self.ptrs.append(own.value)
+                continue
+            peer = C.c_void_p()
+            _check(L.oq_ipc_open((C.c_uint8 * 64).from_buffer_copy(hb), C.byref(peer)))
+            self.ptrs.append(peer.value)
+            self._opened.append(peer)
+        dist.barrier(group=group)
+        self.epoch = 0
+
+    def decode(self, q, cache: KVCache, t_begin, t_end, out=None, stream=None):
+        self.epoch += 1
+        return attention_decode_p2p(q, cache, t_begin, t_end, self.rank, self.nranks, self.ptrs,
+                                    self.epoch, out=out, stream=stream)
+
+    def close(self):
+        L = lib()
+        for peer in self._opened:
+            L.oq_ipc_close(peer)
+        self._opened = []
+        if self._own:
+            L.oq_device_free(self._own)
+            self._own = None
 
 
 def attention_combine(enc_v: Encoder, partials, rows, n_parts, row_stride, part_stride,

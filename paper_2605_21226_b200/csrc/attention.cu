@@ -859,7 +859,8 @@ __device__ __forceinline__ void combine_row(const float* base, int n, float* out
 //  (1) this rank's merged rows of the chunk -> shared staging;
 //  (2) stored into slot `rank` of EVERY rank's exchange buffer — peer memory
 //      over NVLink, mapped into this process (CUDA IPC);
-//  (3) a system-scope release of flag [rank][chunk] = epoch in each buffer;
+//  (3) a system-scope release fence, then flag [rank][chunk] = epoch in
+//      each buffer;
 //  (4) an acquire-spin on this buffer's flags [r][chunk] for every rank r;
 //  (5) the ranks' rows merged in rank order — attention_decode(...,
 //      n_splits = nranks), attention.hpp:60-69 — and finalised into out.
@@ -888,11 +889,14 @@ __device__ __noinline__ void p2p_exchange(const AttnKParams& P, const Seg& it, i
   __syncthreads();
   const size_t flag_off = 2 * (size_t)P.p2p_nranks * rows_total * kPartW * sizeof(float);
   if (tid == 0) {
-    __threadfence_system();
+    // release at system scope, once (the barrier above orders the CTA's row
+    // stores before it; a release fence is cumulative over them), then
+    // relaxed flag stores
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
     for (int r = 0; r < P.p2p_nranks; ++r) {
       uint32_t* fl = reinterpret_cast<uint32_t*>(P.p2p_xbuf[r] + flag_off) +
                      (size_t)P.p2p_rank * P.n_sh + it.sh;
-      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(fl), "r"(P.p2p_epoch) : "memory");
+      asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(fl), "r"(P.p2p_epoch) : "memory");
     }
     const uint32_t* mine = reinterpret_cast<const uint32_t*>(P.p2p_xbuf[P.p2p_rank] + flag_off);
     uint64_t t0;

@@ -1049,6 +1049,12 @@ oq_status oq_device_alloc(size_t bytes, void** ptr) {
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "cudaMalloc");
 }
 
+oq_status oq_device_memset(void* ptr, int value, size_t bytes) {
+  cudaError_t e = cudaMemset(ptr, value, bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return e == cudaSuccess ? OQ_OK : cuda_fail(e, "cudaMemset");
+}
+
 oq_status oq_device_free(void* ptr) {
   cudaError_t e = cudaFree(ptr);
   return e == cudaSuccess ? OQ_OK : cuda_fail(e, "cudaFree");

@@ -4,7 +4,8 @@ Launched by torch.distributed.run with one process per GPU.  Every rank draws
 the same seeded K/V/q (so rank 0 can also build the whole cache), keeps its
 contiguous token slice of each stream in its own cache, and calls the native
 oq_attention_decode_sharded (fused K3 -> this rank's partial -> ONE
-ncclAllGather -> rank-ordered merge).  Rank 0 compares the output with the
+ncclAllGather -> rank-ordered merge), then the same step fused over peer
+memory (P2PExchange / oq_attention_decode_p2p).  Rank 0 compares the output with the
 single-GPU attention_decode over the whole cache and writes the result to the
 file named by argv[1]."""
 import json
@@ -48,14 +49,24 @@ def main():
     outs = [torch.empty_like(got) for _ in range(world)]
     dist.all_gather_object(outs, got.cpu())
     comm.close()
+    # the same step fused over peer memory (CUDA IPC exchange buffers), twice
+    xchg = oq.P2PExchange(mine, Hq)
+    p2p = [xchg.decode(q, mine, 0, per) for _ in range(2)]
+    torch.cuda.synchronize()
+    p2p_outs = [None] * world
+    dist.all_gather_object(p2p_outs, p2p[1].cpu())
+    xchg.close()
     if rank == 0:
         full = oq.KVCache(ek, ev, B, Hkv, T)
         full.pack(kr, vr, T)
         want = oq.attention_decode(q, full).cpu()
         err = ((outs[0] - want).norm(dim=-1) / want.norm(dim=-1)).max().item()
         same = all(torch.equal(o, outs[0]) for o in outs)
+        p2p_err = ((p2p_outs[0] - want).norm(dim=-1) / want.norm(dim=-1)).max().item()
+        p2p_same = all(torch.equal(o, p2p_outs[0]) for o in p2p_outs)
         with open(sys.argv[1], "w") as f:
-            json.dump({"nranks": info[1], "max_rel_err": err, "identical_on_ranks": same}, f)
+            json.dump({"nranks": info[1], "max_rel_err": err, "identical_on_ranks": same,
+                       "p2p_max_rel_err": p2p_err, "p2p_identical_on_ranks": p2p_same}, f)
     dist.destroy_process_group()
 
 

@@ -3,7 +3,7 @@
 * the native oq_attention_decode_sharded with a 2-rank NCCL communicator
   (tests/multirank_worker.py under torch.distributed.run): the output equals
   the single-GPU attention_decode over the whole cache and is bit-identical on
-  both ranks;
+  both ranks; the same for the P2P path over CUDA-IPC exchange buffers;
 * bench.py --gpus 2 --config c5 (it launches its two ranks itself): one JSON
   line whose NCCL communicator reports 2 ranks.
 """
@@ -39,6 +39,8 @@ def test_native_sharded_two_ranks(two_gpus, tmp_path):
     assert r["nranks"] == 2
     assert r["identical_on_ranks"]
     assert r["max_rel_err"] <= 1e-3, r
+    assert r["p2p_identical_on_ranks"]
+    assert r["p2p_max_rel_err"] <= 1e-3, r
 
 
 def test_bench_spawns_two_ranks_c5(two_gpus):
