@@ -528,13 +528,22 @@ def main():
 
     # ---- end to end through the public API with host buffers --------------------
     # Every step uploads its queries from pinned host memory and downloads its
-    # output.  On one GPU the public AttentionPipeline runs the uploads,
-    # kernels and downloads on three streams (double-buffered device q / out),
-    # so copies overlap the neighbouring steps' kernels; the sharded step uses
-    # one stream.  Timed with CUDA events: first on the upload stream, last on
-    # the download stream.
+    # output.  The public AttentionPipeline runs the uploads, kernels and
+    # downloads on three streams (double-buffered device q / out), so copies
+    # overlap the neighbouring steps' kernels; sharded, its step is this
+    # rank's sharded call (the torch.distributed variant keeps one stream).
+    # Timed with CUDA events: first on the upload stream, last on the
+    # download stream.
     out_host = torch.empty((B, Hq, 128), dtype=torch.float32).pin_memory()
-    pipe = None if sharded else oq.AttentionPipeline(cache, Hq, n_splits=splits)
+    pipe = None
+    if not sharded:
+        pipe = oq.AttentionPipeline(cache, Hq, n_splits=splits)
+    elif p2p:
+        pipe = oq.AttentionPipeline(cache, Hq, step=lambda qd, od, s: xchg.decode(
+            qd, cache, 0, cache.tokens, out=od, stream=s))
+    elif native:
+        pipe = oq.AttentionPipeline(cache, Hq, step=lambda qd, od, s: oq.attention_decode_sharded(
+            qd, cache, 0, cache.tokens, comm, n_splits=splits, out=od, stream=s))
 
     def e2e_step():
         if pipe is not None:

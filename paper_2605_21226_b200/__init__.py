@@ -648,9 +648,13 @@ class AttentionPipeline:
     ``run``) has passed.  Every step still moves its own inputs and outputs.
     """
 
-    def __init__(self, cache: KVCache, Hq, n_splits=0, seq_lens=None, device=None):
+    def __init__(self, cache: KVCache, Hq, n_splits=0, seq_lens=None, device=None, step=None):
+        """step: optional callable (q_dev, out_dev, stream) running the
+        attention itself (e.g. a sequence-sharded call); default
+        attention_decode over ``cache``."""
         import torch
         self.cache, self.Hq, self.n_splits, self.seq_lens = cache, Hq, n_splits, seq_lens
+        self.step = step
         dev = device if device is not None else cache.k.device
         D = cache.enc_k.cfg.dim
         self.dev = dev
@@ -679,8 +683,12 @@ class AttentionPipeline:
             self.q_ready[j].record(self.h2d)
         self.compute.wait_event(self.q_ready[j])
         self.compute.wait_event(self.out_free[j])    # step i-2's download of out[j] is done
-        attention_decode(self.q[j], self.cache, n_splits=self.n_splits, seq_lens=self.seq_lens,
-                         out=self.out[j], stream=self.compute)
+        if self.step is not None:
+            with torch.cuda.stream(self.compute):
+                self.step(self.q[j], self.out[j], self.compute)
+        else:
+            attention_decode(self.q[j], self.cache, n_splits=self.n_splits,
+                             seq_lens=self.seq_lens, out=self.out[j], stream=self.compute)
         self.q_free[j].record(self.compute)
         self.out_ready[j].record(self.compute)
         with torch.cuda.stream(self.d2h):
