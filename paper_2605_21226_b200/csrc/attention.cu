@@ -2,26 +2,33 @@
 // OCTOPUS-compressed KV cache on sm_100a (attention.hpp:50-73 semantics, V
 // compressed with the same codec and accumulated in its rotated frame).
 //
-// Per SM, one persistent CTA of 12 warps:
+// Per SM, one persistent CTA (stream-K over all tiles), one launch per step
+// with programmatic dependent launch (griddepcontrol):
 //   * the joint dequant table T[code] = fp16 (rho x, rho y | rho z, 0),
-//     code = ixi | ieta << b_dir | irho << 2 b_dir, sits in shared memory
-//     replicated 16x so the 16 lanes of a half-warp always hit 16 distinct
-//     bank pairs (conflict-free LDS.64 for arbitrary codes);
-//   * each warp streams 32-token tiles of packed K and V codes from HBM into
-//     registers (coalesced; the next tile is prefetched while the current
-//     one is processed);
+//     code = ixi | ieta << b_dir | irho << 2 b_dir, is staged into shared
+//     memory with one 1-D TMA bulk copy as host-built DITHERED replicas (32
+//     at W = 7, 16 at W = 10, 2 at W = 13): a lookup's replica varies with
+//     the lane and the tile, which keeps LDS.64 lookups bank-conflict-free
+//     (W <= 10) and turns the table's fp16 rounding into zero-mean noise;
+//   * each warp streams 32-token tiles of packed K and V codes: 10-bit tiles
+//     straight into registers (8 warps, the next tile prefetched in a second
+//     register image); 7- and 13-bit tiles through a per-warp 2-stage TMA
+//     ring in shared memory (12 / 8 warps, one register image);
 //   * K codes dequantize straight into mma.sync A fragments of S^T = K_hat Q^T
 //     (M = 16 tokens, N = 8 query heads of the GQA group, K = 144 triplet-
-//     permuted dims; Q is permuted identically by the prep kernel);
+//     permuted dims; q is rotated and permuted in the segment prologue);
 //   * online softmax in the log2 domain (q pre-scaled by log2(e)/sqrt(d));
 //     accumulator rescaling is skipped while no running max moves;
 //   * P^T becomes the PV B operand through movmatrix.trans, V codes
 //     dequantize into A fragments of V_hat^T (M = 144 permuted dims, K = 16
-//     tokens), so out^T accumulates in the rotated V frame and the inverse V
-//     rotation runs once per (b, head) in the combine kernel.
+//     tokens), so out^T accumulates in the rotated V frame;
+//   * the CTA that lands a stream's last partial merges the stream's
+//     partials and applies the inverse V rotation (K4 fused), or — sequence-
+//     sharded over peer memory — exchanges the rank's rows with the other
+//     GPUs and merges them (p2p_exchange).
 // Tile formats (see oq_cache_pack): each lane's codes form one contiguous
 // run, so extraction is a static shift+mask (funnel shift across words)
-// folded into the table address: 2 ALU ops + 1 LDS per triplet.
+// folded into the table address: 1-2 ALU ops + 1 LDS per triplet.
 #include <cuda_fp16.h>
 
 #include <cstdint>
@@ -498,10 +505,9 @@ __device__ __forceinline__ void process_tile(WarpState& S, const TileRegs<W, QJL
   // the first two V groups' lookups do not depend on the softmax: issue them
   // before it so their latency overlaps the max/rescale chain (one group:
   // C3/C5/C4 -0.3/-0.8/0 %, two: a further -0/-0.4/-1.3 %, three: slower)
-#ifndef OQ_PREV_QJL
-#define OQ_PREV_QJL 2
-#endif
-  constexpr int kPreV = QJL ? OQ_PREV_QJL : PREV;  // V groups issued before the softmax
+  // V lookup groups issued before the softmax: 2 measured best with and
+  // without QJL and in the ring variants (A/B, r02: 0 / 1 / 2 within 1 %)
+  constexpr int kPreV = PREV;
   uint2 e0[2][2][4];
 #pragma unroll
   for (int gg = 0; gg < kPreV; ++gg)
@@ -1003,9 +1009,6 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
   // warps of a CTA take tiles round-robin, so over a stream every token
   // position meets every residue of t and reads a code through all replicas.
   auto toff_of = [&](size_t t) -> uint32_t {
-#if defined(OQ_NO_DITHER_ROT)
-    return tbase + (((uint32_t)lane & kRepMask) << 3);
-#endif
     return tbase + ((((uint32_t)lane + (uint32_t)t) & kRepMask) << 3);
   };
 
@@ -1046,11 +1049,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
         const size_t tn = tile + (size_t)RING * kAttnWarps;
         if (lane == 0 && tn < it.thi)
           ring_issue<W, QJL>(wr + st * C::STAGE, &s_ring_bar[warp][st], P, it.stream, tn);
-#ifndef OQ_PREV_RING
-#define OQ_PREV_RING 2
-#endif
-        process_tile<W, QJL, OQ_PREV_RING>(S, r, qf, toff_of(tile), (int)(tile * kTileTok), it.lo,
-                                           it.hi, g, c);
+        process_tile<W, QJL>(S, r, qf, toff_of(tile), (int)(tile * kTileTok), it.lo, it.hi, g, c);
         tile += kAttnWarps;
         st = st + 1 == RING ? 0 : st + 1;
       }
