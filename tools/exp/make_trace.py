@@ -42,6 +42,20 @@ rep("""    __syncthreads();
   };
 
   if (!P.streamk) {""")
+# inside the fused query prep (slots 14, 15: the last segment's values)
+rep("""    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) qsw[4 * lane + i] = qkw[4 * lane + i] = 0.f;
+    }
+  }
+  __syncthreads();""", """    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) qsw[4 * lane + i] = qkw[4 * lane + i] = 0.f;
+    }
+  }
+  TR(14);
+  __syncthreads();
+  TR(15);""")
 rep("cudaError_t launch_attention_combine(", """extern "C" int oq_debug_trace(unsigned long long* h) {
   return (int)cudaMemcpyFromSymbol(h, g_trace, sizeof(g_trace));
 }

@@ -12,7 +12,7 @@ L = oq.lib(); L.oq_debug_trace.argtypes = [C.c_void_p]
 buf = np.zeros((148, 16), np.uint64)
 L.oq_debug_trace(buf.ctypes.data)
 t0 = buf[buf[:, 0] > 0, 0].min()
-names = ["start", "staged", "qprep0", "tiles0", "stateout0", "merge0", "atomic0", "end0", "qprep1", "tiles1", "stateout1", "merge1", "atomic1", "end1"]
+names = ["start", "staged", "qprep0", "tiles0", "stateout0", "merge0", "atomic0", "end0", "qprep1", "tiles1", "stateout1", "merge1", "atomic1", "end1", "qp_wht", "qp_sync"]
 rel = np.where(buf > 0, (buf.astype(np.int64) - int(t0)) / 1000.0, np.nan)
 for k, nm in enumerate(names):
     col = rel[:, k]
