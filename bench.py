@@ -166,12 +166,13 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def build_cache(oq, torch, dev, bits, qjl, B, Hkv, T, seed, keep_host=0):
+def build_cache(oq, torch, dev, bits, qjl, B, Hkv, T, seed, keep_host=0, keep_tokens=None):
     """Synthetic Gaussian K/V, compressed by K1 on the device, packed in tiles.
 
     Returns the cache plus (optionally) the first `keep_host` streams' records
-    on the host for the CPU baseline.
+    (their first `keep_tokens` tokens) on the host for the CPU baseline.
     """
+    kt_host = T if keep_tokens is None else min(T, keep_tokens)
     bd, bn = oq.default_bit_split(bits)
     ek = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=1000 + seed, qjl=qjl,
                                    qjl_seed=2000 + seed))
@@ -200,8 +201,8 @@ def build_cache(oq, torch, dev, bits, qjl, B, Hkv, T, seed, keep_host=0):
                                   oq._stream()))
         for i in range(ns):
             if s0 + i < keep_host:
-                host["k"].append(kr[i * T:(i + 1) * T].cpu().numpy())
-                host["v"].append(vr[i * T:(i + 1) * T].cpu().numpy())
+                host["k"].append(kr[i * T:i * T + kt_host].cpu().numpy())
+                host["v"].append(vr[i * T:i * T + kt_host].cpu().numpy())
         del kr, vr
     cache.tokens = T
     torch.cuda.synchronize()
@@ -237,15 +238,18 @@ def kernel_name(bits, qjl):
     return f"attn_partials_kernel<{3 * bits + 1}, {int(qjl)},"
 
 
-def other_configs(oq, torch, dev, peak, main_cfg, steps=20):
+def other_configs(oq, torch, dev, peak, main_cfg, steps=20, ref=None, cpu_secs=5.0):
     """K3 at the BASELINE configs other than the headline one on this GPU (the
     P = 1 point for C5), same method: device-resident cache, library CUDA
-    events around K3, traffic from the committed ncu capture."""
+    events around K3, traffic from the committed ncu capture; with `ref` (the
+    compiled reference) also the reference CPU path on a bounded sample of
+    the same cache (batch entry 0, its first 32K tokens)."""
     res = {}
     for name, (bits, qjl, B, Hq, Hkv, T, scaling, desc) in WORKLOADS.items():
         if name == main_cfg:
             continue
-        cache, _ = build_cache(oq, torch, dev, bits, qjl, B, Hkv, T, seed=7)
+        cache, host = build_cache(oq, torch, dev, bits, qjl, B, Hkv, T, seed=7,
+                                  keep_host=Hkv if ref is not None else 0, keep_tokens=32768)
         q = torch.randn((B, Hq, 128), device=dev, generator=torch.Generator(device=dev).manual_seed(5))
         out = torch.empty((B, Hq, 128), dtype=torch.float32, device=dev)
         step_ms, kern = time_attention(
@@ -258,6 +262,9 @@ def other_configs(oq, torch, dev, peak, main_cfg, steps=20):
                      "frac": nbytes / (kern * 1e-3) / 1e9 / peak,
                      "kernel": kernel_name(bits, qjl),
                      "traffic": ncu_traffic(kernel_name(bits, qjl))}
+        if ref is not None:
+            res[name]["cpu_baseline"] = cpu_attention_baseline(ref, bits, qjl, 7, host, q[0].cpu().numpy(),
+                                                               Hq, Hkv, cpu_secs)
         del cache
         torch.cuda.empty_cache()
     return res
@@ -292,6 +299,41 @@ def cpu_attention_sample(caches, q, threads):
     dt = time.perf_counter() - t0
     assert all(np.all(np.isfinite(o)) for o in outs)
     return dt
+
+
+def cpu_attention_baseline(ref, bits, qjl, seed, host, q0, Hq, Hkv, secs):
+    """The reference CPU path on batch entry 0's streams (records in `host`),
+    query heads q0 [Hq, 128], repeated for ~`secs` s on all host threads."""
+    cores = os.cpu_count() or 1
+    Ts = host["k"][0].shape[0]
+    qs = np.asarray(q0, np.float32).reshape(Hkv, Hq // Hkv, 128)
+    caches, nb = cpu_attention_caches(ref, bits, qjl, seed, host["k"], host["v"])
+    cpu_attention_sample(caches, qs, cores)
+    dts = []
+    t_end = time.perf_counter() + secs
+    while time.perf_counter() < t_end or not dts:
+        dts.append(cpu_attention_sample(caches, qs, cores))
+    tot = sum(dts)
+    return {"value": nb * len(dts) / tot / 1e9, "unit": "GB/s", "cores": cores,
+            "cpu_model": cpu_model(), "kind": "reference",
+            "token_qheads_per_s": Ts * Hq * len(dts) / tot,
+            "sample": f"batch entry 0: {Hkv} KV streams x {Ts} tokens x {Hq} query heads, "
+                      f"V decoded by Encoder::decode + attention_decode per (stream, head); "
+                      f"{len(dts)} repeats, {tot:.1f} s"}
+
+
+def cpu_decode_sample(ref_lib, bits, threads, n=1 << 17, seed=6):
+    """Reference Encoder::decode of n records over `threads` host threads:
+    (keys/s, seconds)."""
+    bd, bn = bits + 1, bits - 1
+    enc = ref_lib.encoder(b_dir=bd, b_nrm=bn)
+    x = np.random.default_rng(seed).standard_normal((n, 128), np.float32)
+    recs = enc.encode_f32(x, threads=threads)
+    enc.decode(recs[:4096], threads=threads)
+    t0 = time.perf_counter()
+    enc.decode(recs, threads=threads)
+    dt = time.perf_counter() - t0
+    return n / dt, dt
 
 
 def cpu_encode_sample(ref_lib, bits, threads, n=1 << 18, seed=5):
@@ -660,42 +702,40 @@ def main():
     if not args.no_compress:
         comp = bench_compress(oq, torch, dev, bits, world, barrier, dist, peak)
 
+    # ---- the reference implementation on this host (CPU baselines) -------------
+    ref = None
+    if keep:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_bind import RefLib
+        ref = RefLib()
+
     # ---- K3 at the other BASELINE configs (C4 QJL, C5 2-bit at P = 1) -----------
     others = None
     if world == 1 and not args.no_other_configs:
         del cache
         torch.cuda.empty_cache()
-        others = other_configs(oq, torch, dev, peak, args.config)
+        others = other_configs(oq, torch, dev, peak, args.config, ref=ref)
 
-    # ---- CPU baseline: the reference implementation on this host ----------------
     cpu = None
-    if keep:
-        sys.path.insert(0, os.path.join(ROOT, "tests"))
-        from oracle_bind import RefLib
-        ref = RefLib()
+    if ref is not None:
         cores = os.cpu_count() or 1
         Ts = min(T, 32768)
-        kr = [h[:Ts] for h in host["k"]]
-        vr = [h[:Ts] for h in host["v"]]
-        qs = q_host[0].numpy().reshape(Hkv, Hq // Hkv, 128)
-        caches, nb = cpu_attention_caches(ref, bits, qjl, rank, kr, vr)
-        cpu_attention_sample(caches, qs, cores)
-        dts = []
-        t_end = time.perf_counter() + 8.0
-        while time.perf_counter() < t_end or not dts:
-            dts.append(cpu_attention_sample(caches, qs, cores))
-        cpu = {"value": nb * len(dts) / sum(dts) / 1e9, "unit": "GB/s", "cores": cores,
-               "cpu_model": cpu_model(), "kind": "reference",
-               "sample": f"batch entry 0: {Hkv} KV streams x {Ts} tokens x {Hq} query heads, "
-                         f"V decoded by Encoder::decode + attention_decode per (stream, head); "
-                         f"{len(dts)} repeats, {sum(dts):.1f} s"}
+        hs = {"k": [h[:Ts] for h in host["k"]], "v": [h[:Ts] for h in host["v"]]}
+        cpu = cpu_attention_baseline(ref, bits, qjl, rank, hs, q_host[0].numpy(), Hq, Hkv, 8.0)
+        full = B * Hkv * T * (rec_bytes(bits, qjl) + rec_bytes(bits, False))
+        cpu["s_per_step_extrapolated"] = full / (cpu["value"] * 1e9)
         if comp is not None:
             kps, dt = cpu_encode_sample(ref, bits, cores)
+            dps, ddt = cpu_decode_sample(ref, bits, cores)
             comp["cpu_baseline"] = {
                 "value": kps, "unit": "tokens/s", "cores": cores, "cpu_model": cpu_model(),
                 "kind": "reference",
                 "sample": f"Encoder::encode of 2^18 fp32 Gaussian keys (local3x3, b={bits}) on "
-                          f"{cores} threads, {dt:.2f} s"}
+                          f"{cores} threads, {dt:.2f} s",
+                "s_per_c2_unit": (1 << 20) / kps,
+                "decode": {"value": dps, "unit": "tokens/s", "s_per_c2_unit": (1 << 20) / dps,
+                           "sample": f"Encoder::decode of 2^17 records (b={bits}) on {cores} "
+                                     f"threads, {ddt:.2f} s"}}
 
     if rank == 0:
         line = {

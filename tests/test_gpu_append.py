@@ -3,7 +3,8 @@
 oq_cache_append compresses one new key/value per (batch, kv head) stream and
 writes it into its token slot of the attention tiles.  Appending a sequence
 token by token must produce the very same tile bytes as compressing the whole
-sequence and packing it (oq_cache_pack), for K (with and without the QJL
+sequence and packing it (oq_cache_pack; those records are checked against the
+oracle's encoder here too), for K (with and without the QJL
 sidecar) and V, with uniform and per-stream (ragged) positions; attention
 over the appended cache then equals attention over the packed one.
 """
@@ -23,7 +24,7 @@ def _encoders(bits, qjl):
 
 
 @pytest.mark.parametrize("bits,qjl", [(3, False), (2, True), (2, False), (4, False), (4, True)])
-def test_append_equals_pack(cuda, bits, qjl):
+def test_append_equals_pack(cuda, orc, bits, qjl):
     import torch
     B, Hkv, T, cap = 2, 2, 70, 96
     n = B * Hkv
@@ -35,6 +36,15 @@ def test_append_equals_pack(cuda, bits, qjl):
     kr = ek.compress(k.reshape(-1, 128)).reshape(n, T, -1)
     vr = ev.compress(v.reshape(-1, 128)).reshape(n, T, -1)
     packed.pack(kr, vr, T)
+    # the packed records are the oracle's (so the appended tiles are pinned to
+    # the CPU encoder, not only to the GPU compress path)
+    bd, bn = oq.default_bit_split(bits)
+    ok = orc.encoder(b_dir=bd, b_nrm=bn, rotation_seed=21, qjl=qjl, qjl_seed=22)
+    ov = orc.encoder(b_dir=bd, b_nrm=bn, rotation_seed=23)
+    assert np.array_equal(ok.encode_f32(k.reshape(-1, 128).cpu().numpy()),
+                          kr.reshape(n * T, -1).cpu().numpy())
+    assert np.array_equal(ov.encode_f32(v.reshape(-1, 128).cpu().numpy()),
+                          vr.reshape(n * T, -1).cpu().numpy())
     app = oq.KVCache(ek, ev, B, Hkv, cap)
     for t in range(T):
         app.append(k[:, t].reshape(B, Hkv, 128), v[:, t].reshape(B, Hkv, 128))
