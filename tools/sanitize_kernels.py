@@ -52,6 +52,21 @@ for qjl in (False, True):
     oq.attention_decode(q, c3)
     oq.attention_decode(q, c3, n_splits=3)
     oq.attention_partials(q, c3, 100, 1500)
+# 13-bit tiles (b = 4: two-replica table, 8-warp TMA ring), with and without QJL
+for qjl in (False, True):
+    e4k = oq.Encoder(oq.CodecConfig(b_dir=5, b_nrm=3, qjl=qjl, rotation_seed=31))
+    e4v = oq.Encoder(oq.CodecConfig(b_dir=5, b_nrm=3, rotation_seed=32))
+    c4 = oq.KVCache(e4k, e4v, B, Hkv, 700)
+    c4.pack(e4k.compress(torch.randn((B * Hkv * 700, 128), device=dev, generator=g)),
+            e4v.compress(torch.randn((B * Hkv * 700, 128), device=dev, generator=g)), 700)
+    oq.attention_decode(q, c4)
+    oq.attention_decode(q, c4, seq_lens=torch.tensor([650, 90], dtype=torch.int32, device=dev))
+# ragged lengths on the 10-bit tiles, and the fused peer-memory exchange with
+# one rank (stores, system fence, flag, acquire-spin, merge; two epochs)
+oq.attention_decode(q, cache, seq_lens=torch.tensor([T, 17], dtype=torch.int32, device=dev))
+xb = torch.zeros(oq.p2p_exchange_bytes(cache, q.shape[1], 1), dtype=torch.uint8, device=dev)
+for ep in (1, 2):
+    oq.attention_decode_p2p(q, cache, 0, cache.tokens, 0, 1, [xb], ep)
 # the exact fp64 per-key API (exact_api.cu)
 for cfg in (oq.CodecConfig(b_dir=4, b_nrm=2), oq.CodecConfig(b_dir=5, b_nrm=3, qjl=True),
             oq.CodecConfig(dim=64, b_dir=3, b_nrm=1)):
