@@ -150,6 +150,19 @@ def test_pack_keys_matches_reference_blob(ref, cuda, orc):
     assert blob[20:] == want.tobytes()
 
 
+@pytest.mark.parametrize("qjl", [False, True])
+def test_empty_batches(cuda, qjl):
+    """Zero keys in, zero records out (and back): no launch, no error, the way
+    the reference's encode/decode loops simply do nothing."""
+    import torch
+    enc = oq.Encoder(oq.CodecConfig(b_dir=4, b_nrm=2, qjl=qjl))
+    r = enc.compress(torch.zeros((0, 128), device=cuda))
+    assert r.shape == (0, enc.record_bytes)
+    d = enc.decode(r)
+    assert d.shape == (0, 128)
+    torch.cuda.synchronize()
+
+
 def test_rejects_dimension_mismatch(cuda):
     import torch
     with pytest.raises(ValueError):
