@@ -242,6 +242,13 @@ __device__ __forceinline__ uint32_t sign_pair(uint32_t nw, int sigma) {
   return ((nw << (15 - sigma)) & 0x80008000u) | 0x3C003C00u;
 }
 
+// Word k (0..3) of a 4-word mask held in kernel parameters, by selects: a
+// runtime index into a parameter array would copy it to local memory.
+__device__ __forceinline__ uint32_t word4(const uint32_t (&m)[4], int k) {
+  const uint32_t a = (k & 1) ? m[1] : m[0], b = (k & 1) ? m[3] : m[2];
+  return (k & 2) ? b : a;
+}
+
 __device__ __forceinline__ void wht128_lane4(float (&y)[4], int lane) {
   // normalized-free WHT over 128 values, 4 consecutive per lane
   {
@@ -765,7 +772,7 @@ __device__ __forceinline__ void seg_qprep(uint32_t (&qf)[QF], const AttnKParams&
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int e = 4 * lane + i;
-        if ((P.smask[e >> 5] >> (e & 31)) & 1u) y[i] = -y[i];
+        if ((word4(P.smask, e >> 5) >> (e & 31)) & 1u) y[i] = -y[i];
       }
       wht128_lane4(y, lane);
       const float s_attn = P.inv_sqrt_d * P.inv_sqrt_d * log2e;
@@ -777,7 +784,7 @@ __device__ __forceinline__ void seg_qprep(uint32_t (&qf)[QF], const AttnKParams&
         for (int i = 0; i < 4; ++i) {
           const int e = 4 * lane + i;
           const float v = y[i] * P.inv_sqrt_d;
-          z[i] = ((P.qmask[e >> 5] >> (e & 31)) & 1u) ? -v : v;
+          z[i] = ((word4(P.qmask, e >> 5) >> (e & 31)) & 1u) ? -v : v;
         }
         wht128_lane4(z, lane);
         const float s_sk = P.inv_sqrt_d * P.inv_sqrt_d * log2e * sqrtf(1.5707963267948966f / 128.f);
@@ -814,15 +821,42 @@ __device__ __forceinline__ void combine_row(const float* base, int n, float* out
                                             size_t stride = kPartW) {
   const float NEG_INF = -__int_as_float(0x7f800000);
   float M = NEG_INF;
-  for (int i = lane; i < n; i += 32) {
-    const float2 ml = *reinterpret_cast<const float2*>(base + (size_t)i * stride);
-    if (ml.y > 0.f) M = fmaxf(M, ml.x);
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
   float L = 0.f, y[4] = {0.f, 0.f, 0.f, 0.f};
-  // the parts were just written by other CTAs (L2): request a batch of them
-  // before consuming it, instead of one dependent round trip per part
+  // the parts were just written by other CTAs (L2).  Up to 8 parts (the
+  // usual count): ONE batch of loads, the maximum taken from it, then the
+  // same in-order sums — one L2 round trip on the launch's critical path
+  // instead of three
+  constexpr int NB1 = 8;
+  if (n >= 1 && n <= NB1) {
+    float2 ml[NB1];
+    float4 a4[NB1];
+#pragma unroll
+    for (int j = 0; j < NB1; ++j) {  // past the end: re-read the last part, skipped below
+      const size_t i = (size_t)min(j, n - 1);
+      ml[j] = *reinterpret_cast<const float2*>(base + i * stride);
+      a4[j] = *reinterpret_cast<const float4*>(base + i * stride + 4 + 4 * lane);
+    }
+#pragma unroll
+    for (int j = 0; j < NB1; ++j)
+      if (j < n && ml[j].y > 0.f) M = fmaxf(M, ml[j].x);
+#pragma unroll
+    for (int j = 0; j < NB1; ++j)
+      if (j < n && ml[j].y > 0.f) {  // in part order
+        const float f = ex2(ml[j].x - M);
+        L += ml[j].y * f;
+        y[0] += a4[j].x * f; y[1] += a4[j].y * f; y[2] += a4[j].z * f; y[3] += a4[j].w * f;
+      }
+    n = 0;  // done: skip the general loop below
+  } else {
+    for (int i = lane; i < n; i += 32) {
+      const float2 ml = *reinterpret_cast<const float2*>(base + (size_t)i * stride);
+      if (ml.y > 0.f) M = fmaxf(M, ml.x);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(kFull, M, o));
+  }
+  // more parts: batches of them requested before they are consumed, instead
+  // of one dependent round trip per part
   constexpr int NB = 4;
   for (int i0 = 0; i0 < n; i0 += NB) {
     float2 ml[NB];
@@ -855,7 +889,7 @@ __device__ __forceinline__ void combine_row(const float* base, int n, float* out
   for (int i = 0; i < 4; ++i) {
     const int e = 4 * lane + i;
     const float v = y[i] * inv_sqrt_d;
-    r[i] = ((vmask[e >> 5] >> (e & 31)) & 1u) ? -v : v;
+    r[i] = ((word4(vmask, e >> 5) >> (e & 31)) & 1u) ? -v : v;
   }
   *reinterpret_cast<float4*>(out + 4 * lane) = make_float4(r[0], r[1], r[2], r[3]);
 }
@@ -1156,7 +1190,7 @@ __global__ void qprep_kernel(QPrepParams P) {
     for (int i = 0; i < 4; ++i) {
       const int e = 4 * lane + i;
       const float v = q[e];
-      y[i] = ((P.smask[e >> 5] >> (e & 31)) & 1u) ? -v : v;
+      y[i] = ((word4(P.smask, e >> 5) >> (e & 31)) & 1u) ? -v : v;
     }
     wht128_lane4(y, lane);
     const float s_attn = P.inv_sqrt_d * P.inv_sqrt_d * log2e;  // rotation norm x 1/sqrt(d) x log2e
@@ -1168,7 +1202,7 @@ __global__ void qprep_kernel(QPrepParams P) {
       for (int i = 0; i < 4; ++i) {
         const int e = 4 * lane + i;
         const float v = y[i] * P.inv_sqrt_d;  // q_rot
-        z[i] = ((P.qmask[e >> 5] >> (e & 31)) & 1u) ? -v : v;
+        z[i] = ((word4(P.qmask, e >> 5) >> (e & 31)) & 1u) ? -v : v;
       }
       wht128_lane4(z, lane);
       const float s_sk = P.inv_sqrt_d * P.inv_sqrt_d * log2e * sqrtf(1.5707963267948966f / 128.f);
@@ -1262,7 +1296,7 @@ __global__ void combine_kernel(CombineParams P) {
   for (int i = 0; i < 4; ++i) {
     const int e = 4 * lane + i;
     const float v = y[i] * P.inv_sqrt_d;
-    r[i] = ((P.smask[e >> 5] >> (e & 31)) & 1u) ? -v : v;
+    r[i] = ((word4(P.smask, e >> 5) >> (e & 31)) & 1u) ? -v : v;
   }
   *reinterpret_cast<float4*>(P.out + (size_t)row * 128 + 4 * lane) = make_float4(r[0], r[1], r[2], r[3]);
 }
