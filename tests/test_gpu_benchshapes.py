@@ -263,3 +263,18 @@ def test_b4_tiles_long_context(orc, cuda):
     q = torch.randn((B, Hq, 128), generator=torch.Generator().manual_seed(95))
     got = oq.attention_decode(q.to(cuda), cache).cpu().numpy()
     compare(got, oracle_rows(ok, ov, host, q.numpy(), Hkv, Hq // Hkv))
+
+
+@pytest.mark.parametrize("bits", [3, 4])
+def test_qjl_keys_long_context(orc, cuda, bits):
+    """QJL keys on the 10- and 13-bit tiles (b = 3, 4) at a 64K-token context:
+    the sign-sketch MMA chain and the dithered tables over a long softmax
+    average, against the reference."""
+    import torch
+    B, Hq, Hkv, T = 1, 14, 2, 65536
+    cache, host, ok, ov = build_bench_cache(orc, cuda, bits, True, B, Hkv, T, [0, 1],
+                                            seed=40 + bits)
+    check_codes(ok, ov, host, n_check=1 << 13)
+    q = torch.randn((B, Hq, 128), generator=torch.Generator().manual_seed(96 + bits))
+    got = oq.attention_decode(q.to(cuda), cache).cpu().numpy()
+    compare(got, oracle_rows(ok, ov, host, q.numpy(), Hkv, Hq // Hkv))
