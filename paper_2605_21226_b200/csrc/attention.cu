@@ -10,10 +10,11 @@
 //     at W = 7, 16 at W = 10, 2 at W = 13): a lookup's replica varies with
 //     the lane and the tile, which keeps LDS.64 lookups bank-conflict-free
 //     (W <= 10) and turns the table's fp16 rounding into zero-mean noise;
-//   * each warp streams 32-token tiles of packed K and V codes: 10-bit tiles
-//     straight into registers (8 warps, the next tile prefetched in a second
-//     register image); 7- and 13-bit tiles through a per-warp 2-stage TMA
-//     ring in shared memory (12 / 8 warps, one register image);
+//   * each warp streams 32-token tiles of packed K and V codes through a
+//     per-warp 2-stage TMA ring in shared memory (12 warps at 7 and 10 bits,
+//     8 at 13 bits, one register image); 10-bit tiles with QJL keys straight
+//     into registers (8 warps, the next tile prefetched in a second register
+//     image);
 //   * K codes dequantize straight into mma.sync A fragments of S^T = K_hat Q^T
 //     (M = 16 tokens, N = 8 query heads of the GQA group, K = 144 triplet-
 //     permuted dims; q is rotated and permuted in the segment prologue);
@@ -1773,13 +1774,15 @@ cudaError_t launch_attention_partials(const OqCodecParams& pk, const OqCodecPara
     return e ? atoi(e) : -1;
   }();
   // measured defaults (tools/exp/abn.sh, r02; a 3-stage ring measured the
-  // same as 2 stages): the byte-coded 2-bit tiles
-  // (W = 7, C4/C5) run 12 warps fed by a 2-stage TMA ring (C4 -10 %, C5
-  // -1.7 %); the 10-bit tiles (C3) keep 8 warps with register prefetch (the
-  // ring costs them 2-10 %); the 13-bit tiles (b = 4) need the ring's single
+  // same as 2 stages): 12 warps fed by a 2-stage TMA ring for the byte-coded
+  // 2-bit tiles (W = 7, C4/C5: C4 -10 %, C5 -1.7 % against 8 warps with
+  // register prefetch) and, since the round-2 kernel changes, for the 10-bit
+  // tiles too (C3 147.3 -> 144.0 us, A/B); 10-bit tiles with QJL keys (the
+  // 12-warp ring does not fit their shared memory) keep 8 warps with
+  // register prefetch; the 13-bit tiles (b = 4) need the ring's single
   // register image (8 warps)
-  const int ring = ring_env >= 0 ? ring_env : (W == 10 ? 0 : 2);
-  const int nw = nw_env > 0 ? nw_env : (ring && W == 7 ? 12 : 8);
+  const int ring = ring_env >= 0 ? ring_env : (W == 10 && pk.qjl ? 0 : 2);
+  const int nw = nw_env > 0 ? nw_env : (ring && W <= 10 ? 12 : 8);
   auto launch = [&](auto w_tag, auto q_tag) -> cudaError_t {
     constexpr int WW = decltype(w_tag)::value;
     constexpr bool QQ = decltype(q_tag)::value;
