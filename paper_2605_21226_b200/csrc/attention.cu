@@ -911,7 +911,24 @@ __device__ __forceinline__ void combine_row(const float* base, int n, float* out
 // epoch's parity: a rank can start the next call while a slower one still
 // reads this call's rows), then u32 flags [nranks][n_sh] (zeroed once; epochs
 // increase per call, and a flag that has already moved on counts as arrived).
-__device__ __noinline__ void p2p_exchange(const AttnKParams& P, const Seg& it, int nparts,
+// The fields p2p_exchange reads.  Passing the kernel parameters themselves
+// by reference to this out-of-line function makes every thread copy the
+// whole parameter block to local memory at kernel entry (~26 MB of DRAM
+// writes per C3 launch); the QJL kernels pass this copied subset instead
+// (C4 -1 %), while for the others every way of avoiding the copy measured
+// 2-3 % slower tile-loop code, so they keep it.
+struct P2PView {
+  float* partials;
+  float* out;
+  uint8_t* p2p_xbuf[8];
+  uint32_t vmask[4];
+  float inv_sqrt_d;
+  int G, B, Hq, n_parts, n_sh, p2p_nranks, p2p_rank;
+  uint32_t p2p_epoch;
+};
+
+template <class PV>
+__device__ __noinline__ void p2p_exchange(const PV& P, const Seg& it, int nparts,
                                           float* stage, int tid, int warp, int lane, int nwarps) {
   const int nh = min(8, P.G - 8 * it.hc);
   const size_t rows_total = (size_t)P.B * P.Hq;
@@ -1129,7 +1146,27 @@ __global__ void __launch_bounds__(kAttnWarps * 32, 1) attn_partials_kernel(const
       }
       __syncthreads();
       if (s_last && P.p2p_nranks > 0) {
-        p2p_exchange(P, it, nparts, qs, tid, warp, lane, kAttnWarps);
+        if constexpr (QJL) {
+          P2PView V;
+          V.partials = P.partials;
+          V.out = P.out;
+#pragma unroll
+          for (int r = 0; r < 8; ++r) V.p2p_xbuf[r] = P.p2p_xbuf[r];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) V.vmask[i] = P.vmask[i];
+          V.inv_sqrt_d = P.inv_sqrt_d;
+          V.G = P.G;
+          V.B = P.B;
+          V.Hq = P.Hq;
+          V.n_parts = P.n_parts;
+          V.n_sh = P.n_sh;
+          V.p2p_nranks = P.p2p_nranks;
+          V.p2p_rank = P.p2p_rank;
+          V.p2p_epoch = P.p2p_epoch;
+          p2p_exchange(V, it, nparts, qs, tid, warp, lane, kAttnWarps);
+        } else {
+          p2p_exchange(P, it, nparts, qs, tid, warp, lane, kAttnWarps);
+        }
       } else if (s_last) {
         for (int w = warp; w < 8; w += kAttnWarps) {
           if (8 * it.hc + w >= P.G) continue;

@@ -21,10 +21,10 @@ import paper_2605_21226_b200 as oq
 pytestmark = pytest.mark.gpu
 
 
-def _ranks_setup(cuda, bits, B, Hkv, T, P):
+def _ranks_setup(cuda, bits, B, Hkv, T, P, qjl=False):
     import torch
     bd, bn = oq.default_bit_split(bits)
-    ek = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=51))
+    ek = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=51, qjl=qjl, qjl_seed=53))
     ev = oq.Encoder(oq.CodecConfig(b_dir=bd, b_nrm=bn, rotation_seed=52))
     g = torch.Generator(device=cuda).manual_seed(7)
     k = torch.randn((B * Hkv, T, 128), device=cuda, generator=g)
@@ -43,11 +43,12 @@ def _ranks_setup(cuda, bits, B, Hkv, T, P):
     return full, caches, per
 
 
-@pytest.mark.parametrize("bits,P", [(3, 2), (2, 3), (3, 4)])
-def test_p2p_exchange_emulated_ranks(cuda, bits, P):
+@pytest.mark.parametrize("bits,P,qjl", [(3, 2, False), (2, 3, False), (3, 4, False), (2, 2, True),
+                                        (3, 3, True)])
+def test_p2p_exchange_emulated_ranks(cuda, bits, P, qjl):
     import torch
     B, Hq, Hkv, T = 2, 14, 2, 6144
-    full, caches, per = _ranks_setup(cuda, bits, B, Hkv, T, P)
+    full, caches, per = _ranks_setup(cuda, bits, B, Hkv, T, P, qjl)
     sms = torch.cuda.get_device_properties(cuda).multi_processor_count
     nbytes = oq.p2p_exchange_bytes(caches[0], Hq, P)
     xbufs = [torch.zeros(nbytes, dtype=torch.uint8, device=cuda) for _ in range(P)]
