@@ -733,7 +733,8 @@ static oq_status run_partials(const oq_codec* ck, const oq_codec* cv, const oq_a
   // one launch when the per-stream counters fit: q prep and the final merge
   // run inside the attention kernel
   const size_t n_sh = (size_t)sh->B * sh->Hkv * ((sh->Hq / sh->Hkv + 7) / 8);
-  const bool fuse = fused_out && n_sh * 4 <= kCounterBytes && !getenv("OQ_ATTN_UNFUSED");
+  static const bool unfused = getenv("OQ_ATTN_UNFUSED") != nullptr;  // comparison runs
+  const bool fuse = fused_out && n_sh * 4 <= kCounterBytes && !unfused;
   cudaError_t e = cudaSuccess;
   if (p2p && !fuse) return fail(OQ_ERR_UNSUPPORTED, "P2P sharding needs the fused attention kernel");
   if (fuse) {
