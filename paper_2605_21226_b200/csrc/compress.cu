@@ -355,7 +355,10 @@ __global__ void __launch_bounds__(32 * kSmallWarps) compress_small_kernel(
 // and norm fields into the record in place — the pass masks every field to
 // its width, so the other fields are already final.  Records of different
 // keys may share a 32-bit word, hence atomic clear + set on disjoint bits.
-constexpr int kFixWarps = 8, kFixKeys = 16, kFixQ = 896;
+// 4 CTAs per SM in the (persistent, strided) grid: b = 3 fixup 518 -> 510 us
+// for the whole compress (A/B; b = 2 +0.8 %, b = 4 unchanged; 8 keys per
+// warp-round, 4 warps, 6 or 8 CTAs per SM were no better)
+constexpr int kFixWarps = 8, kFixKeys = 16, kFixQ = 896, kFixCtasPerSm = 4;
 
 struct FixTriplet {
   double t0, t1, t2;
@@ -495,7 +498,8 @@ cudaError_t launch_compress_fixup(const OqCodecParams& p, const void* x, int dty
   const int sm = kFixWarps * kFixKeys * 128 * 4;
   cudaError_t e = set_smem_once(compress_fixup_kernel, sm);
   if (e != cudaSuccess) return e;
-  compress_fixup_kernel<<<2 * num_sms, 32 * kFixWarps, sm, st>>>(p, x, dtype, out, flags, flag_cnt);
+  compress_fixup_kernel<<<kFixCtasPerSm * num_sms, 32 * kFixWarps, sm, st>>>(p, x, dtype, out, flags,
+                                                                            flag_cnt);
   return cudaGetLastError();
 }
 
