@@ -1610,10 +1610,6 @@ __global__ void __launch_bounds__(32 * kAppendWarps) append_fused_kernel(
   __shared__ double row_s[kAppendWarps][132];
   __shared__ uint32_t rec_s[kAppendWarps][kRecWords];
   __shared__ uint32_t run_s[kAppendWarps][32][21];
-  // the attention launch that follows (programmatic dependent launch) may
-  // start now on the SMs this small grid leaves free: it stages its table
-  // and then waits (griddepcontrol.wait) for this grid to complete
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, role = blockIdx.y;
   const size_t s = blockIdx.x * (size_t)kAppendWarps + wib;
   if (s >= n_streams) return;
