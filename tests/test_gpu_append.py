@@ -114,3 +114,35 @@ def test_append_records_and_bf16(cuda, qjl):
         assert torch.equal(a, b), s
         assert torch.equal(app.v[s * per_v + vt:s * per_v + 2 * vt],
                            ref.v[s * per_v + vt:s * per_v + 2 * vt]), s
+
+
+def test_append_then_attention_back_to_back(cuda):
+    """Decode-step pattern with no host synchronisation between the append
+    and the attention launch that reads it (the attention kernel is launched
+    with programmatic dependent launch): every step's output equals the same
+    step recomputed after a device synchronisation."""
+    import torch
+    B, Hkv, cap = 2, 2, 4096
+    ek, ev = _encoders(3, False)
+    cache = oq.KVCache(ek, ev, B, Hkv, cap)
+    g = torch.Generator(device=cuda).manual_seed(3)
+    T0 = 3000
+    cache.pack(ek.compress(torch.randn((B * Hkv * T0, 128), device=cuda, generator=g)).reshape(
+        B * Hkv, T0, -1), ev.compress(torch.randn((B * Hkv * T0, 128), device=cuda,
+                                                  generator=g)).reshape(B * Hkv, T0, -1), T0)
+    q = torch.randn((B, 7 * Hkv, 128), device=cuda, generator=g)
+    ks = torch.randn((40, B, Hkv, 128), device=cuda, generator=g)
+    vs = torch.randn((40, B, Hkv, 128), device=cuda, generator=g)
+    outs = []
+    for t in range(40):  # back to back: append, attention, append, attention, ...
+        cache.append(ks[t], vs[t])
+        outs.append(oq.attention_decode(q, cache).clone())
+    torch.cuda.synchronize()
+    # every step's output equals attention over the final cache read up to
+    # that step's length (same T, so the same work split), computed after a
+    # synchronisation: later appends leave earlier tokens' codes unchanged
+    for t in range(40):
+        torch.cuda.synchronize()
+        want = oq.attention_decode(q, cache, T=T0 + t + 1)
+        torch.cuda.synchronize()
+        assert torch.equal(want, outs[t]), t
