@@ -251,6 +251,25 @@ oq_status build_codec(const oq_config* cfg, const oqh::Book& xi, const oqh::Book
       }
       dirs32[4 * (a * K + b) + 3] = 0.f;
     }
+  // The largest distance between two directions of one 3x3 window of
+  // cells (valid cells only), for the certified argmax in compress_fast.cu;
+  // rounded up to fp32 with margin.
+  {
+    double dmax = 0.0;
+    for (int a = 0; a < (int)K; ++a)
+      for (int b = 0; b < (int)K; ++b)
+        for (int a2 = a; a2 <= a + 2 && a2 < (int)K; ++a2)
+          for (int b2 = b - 2; b2 <= b + 2; ++b2) {
+            if (b2 < 0 || b2 >= (int)K || (a2 == a && b2 <= b)) continue;
+            double d2 = 0.0;
+            for (int j = 0; j < 3; ++j) {
+              const double d = dirs64[3 * (a * K + b) + j] - dirs64[3 * (a2 * K + b2) + j];
+              d2 += d * d;
+            }
+            dmax = std::max(dmax, std::sqrt(d2));
+          }
+    p.dwin = static_cast<float>(std::min(2.0, dmax * (1.0 + 1e-6) + 1e-7));
+  }
   std::vector<float> rho32(KR);
   for (uint32_t i = 0; i < KR; ++i) rho32[i] = static_cast<float>(rho.centroids[i]);
   // the attention kernel's dithered replica table (tile formats exist for W <= 13)

@@ -28,6 +28,9 @@ struct OqCodecParams {
   const uint2* jointrep;   // attention table: 2^W codes x REP dithered fp16 replicas of
                            // (rho*x, rho*y | rho*z, 0), W = 2 b_dir + b_nrm, REP = 32 for
                            // W <= 8 else 16 (joint_replicas(), capi.cpp; attention.cu)
+  float dwin;              // >= max |n_a - n_b| over the direction pairs of any 3x3 window
+                           // (host, fp64, rounded up): certifies the local3x3 argmax
+                           // by the score DIFFERENCE's error, |dt| * |n_a - n_b|
   const uint32_t* xi_lut;  // 1024-cell index brackets over [-1, 1] (compress quantize)
   const uint32_t* rho_lut; // 1024-cell index brackets over [0, 1]
 };

@@ -337,7 +337,11 @@ __global__ void __launch_bounds__(CFS<BD, BN, QJL>::NW * 32, 1)
           // score error: ||dt|| <= Et (rotation) + |t| u/2 (fp32 table) + 3u |t|
           // (dot rounding), with |t| <= l1
           const float gs = (E0 + 5.53f * U * l1) * 1.001f;
-          okt = okt && (b1 - b2 > 2.002f * gs);
+          // the best beats every other candidate c by more than the error of
+          // the score difference: |dt| |n_best - n_c| (<= Et dwin, dwin
+          // bounding the direction distances within any window) plus the
+          // rounding of the two fp32 dot products and table entries (7u |t|)
+          okt = okt && (b1 - b2 > (p.dwin * (E0 + 2.02f * U * l1) + 7.02f * U * l1) * 1.002f);
           ix = sx + (wi >> 2) - 1;
           iy = sy + (wi & 3) - 1;
           rv = b1;
