@@ -303,11 +303,18 @@ __global__ void __launch_bounds__(CFS<BD, BN, QJL>::NW * 32, 1)
         // Et = E0 + 2.01u |t| <= E0 + 2.01u l1.  xi = t0 / l1 (or 1 - |t1| / l1):
         // |d xi| <= (|dt0| + |xi| |dl1|) / l1 <= (1 + sqrt 3) Et / l1, plus <= 8u
         // of fp32 rounding and u for the fp32 boundaries
-        const float gx = (2.74f * E0 * il + 5.51f * U + 9.f * U) * 1.001f;
         const bool up = pad || t2 >= 0.f;  // octahedral.hpp:28 (pad: pz = 0 exactly)
         // hemisphere and, below it, sgn(px), sgn(py) (octahedral.hpp:29-30):
         // |t_i| > E0 + 2.01u |t_i| is implied by |t_i| > 1.0001 E0
         const float es = 1.0001f * E0;
+        // When the signs of t0 and t1 cannot flip under the rotation error
+        // (|t_i| > es; t2's sign is certified below, the pad's t2 is exactly
+        // 0), l1 is linear in dt and xi' - xi = (w . dt) / l1' with
+        // |w|^2 = (1 - |xi|)^2 + 2 xi^2 <= 2: the factor (1 + sqrt 3) drops
+        // to sqrt 2 (the same for eta, and in the lower hemisphere with t1
+        // and t0 swapped)
+        const bool sst = a0 > es && a1 > es;
+        const float gx = ((sst ? 1.415f : 2.74f) * E0 * il + (sst ? 2.85f : 5.51f) * U + 9.f * U) * 1.001f;
         okt = l1 > 1e-6f && (pad || a2 > es) && (up || (a0 > es && a1 > es));
         const float xi = up ? t0 * il : copysignf(1.f - a1 * il, t0);
         const float eta = up ? t1 * il : copysignf(1.f - a0 * il, t1);
